@@ -1,0 +1,177 @@
+/*
+ * quakescan-b200 — C ABI of the B200 (sm_100a) hot path of the FAST-style
+ * waveform similarity search (reference: quakescan 0.1.0, arXiv 1803.09835).
+ *
+ * Every entry point takes plain pointers and sizes (no torch or CUDA types in
+ * the signatures; `stream` is a cudaStream_t passed as void*, NULL = legacy
+ * default stream).  Pointers named *_dev are device memory; the caller owns
+ * every buffer (outputs are preallocated by the caller, scratch comes from a
+ * caller workspace sized by the matching *_bytes query).  Calls are
+ * stream-ordered and never synchronize the device unless documented.
+ *
+ * Return value: QS_OK (0) or an error code; qs_last_error() returns the text
+ * of the last error on the calling thread.  The Python host layer maps
+ * QS_ERR_ARG -> ParameterError, QS_ERR_DATA -> DataError, QS_ERR_OOM ->
+ * MemoryError, QS_ERR_CUDA -> RuntimeError (reference error taxonomy,
+ * pkg/src/quakescan/errors.py:1-29).  Nothing aborts the process.
+ *
+ * Reference interfaces replaced are cited per function as file:line under
+ * /root/reference/pkg/src/quakescan/.
+ */
+#ifndef QUAKESCAN_B200_H
+#define QUAKESCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QS_OK 0
+#define QS_ERR_ARG 1   /* bad shape / range / parameter      -> ParameterError */
+#define QS_ERR_OOM 2   /* device allocation failed             -> MemoryError    */
+#define QS_ERR_CUDA 3  /* CUDA runtime / launch failure        -> RuntimeError   */
+#define QS_ERR_DATA 4  /* input data unusable (e.g. bit >= d)  -> DataError      */
+
+/* ---------------------------------------------------------------- library */
+const char* qs_version(void);
+const char* qs_last_error(void);
+/* Writes "name|sm_major.minor|n_sms|hbm_bytes" of the current device. */
+int qs_device_info(char* buf, size_t len);
+
+/* ------------------------------------------------------------ Min-Max hash */
+
+/* values_dev[x * n_funcs + j] = fmix64(((x + 1) * GOLDEN64) ^ (seed + j)).
+ * Replaces minmax_hash.gen_hash_mapping (minmax_hash.py:73-90). */
+int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs,
+                        uint64_t seed, void* stream);
+
+/* Probe plan of a mapping: for every hash column the element indices in
+ * ascending value order plus the sorted values (rank-major layout).  Built
+ * once per mapping; consumed by qs_minmax_signatures. */
+size_t qs_minmax_plan_bytes(uint32_t d, uint32_t n_funcs);
+int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs,
+                   void* plan_dev, void* stream);
+
+/* Min-Max signatures of rows [0, n) of bits_dev (n, K) uint32 -> out_dev (n, t)
+ * uint64, bit-identical to _sigcore.gen_signatures_range (_sigcore.pyx:32-85):
+ * out[r, i] = fold(min over set bits of V[:, i*kh + j] for j < kh, then max ...).
+ * A bit index >= d sets *bad_dev (uint32, device) to 1 and that row is
+ * unspecified (the Python layer validates first, minmax_hash.py:107-108). */
+int qs_minmax_signatures(const uint32_t* bits_dev, uint64_t n, uint32_t K,
+                         const void* plan_dev, uint32_t d, uint32_t t, uint32_t k_half,
+                         uint64_t* out_dev, uint32_t* bad_dev, void* stream);
+
+/* Same computation, table-major output for the search: keys_dev (t, n) uint64
+ * holds mix64(sig) (a bijection of the signature word, so bucket equality is
+ * unchanged) and tags_dev (n, 16, ceil(t/32)) uint32 the bit-sliced 16-bit
+ * tags used for exact first-colliding-table dedup.  sigs_dev (n, t) may be
+ * NULL when the row-major signatures are not wanted. */
+int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K,
+                                const void* plan_dev, uint32_t d, uint32_t t,
+                                uint32_t k_half, uint64_t* sigs_dev, uint64_t* keys_dev,
+                                uint32_t* tags_dev, uint32_t* bad_dev, void* stream);
+
+/* HOST-buffer drop-in for the reference's native plugin point
+ * `_core.gen_signatures_range(bits, values, t, k_half, out, start, stop)`
+ * (minmax_hash.py:24-30 selects it; _sigcore.pyx:32-36 defines it): fills
+ * out[start:stop] (n_rows, t) from bits (n_rows, K) and values (d, F).
+ * Stages through device memory on an internal stream; synchronous. */
+int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
+                            const uint64_t* values, uint32_t d, uint32_t F,
+                            int32_t t, int32_t k_half, uint64_t* out,
+                            uint64_t start, uint64_t stop);
+
+/* ------------------------------------------------------------- LSH search
+ * The search (lsh_search.search_signatures, lsh_search.py:222-303) runs as the
+ * stage sequence below, orchestrated by the Python host layer which owns all
+ * buffers.  Layout: keys (t, n) uint64 table-major mixed signature words;
+ * tags (n, 16, W) uint32, W = ceil(t/32). */
+
+/* Row-major signatures (n, t) -> keys (t, n) + tags.  Used when the caller
+ * hands in signatures (search_signatures) rather than bits. */
+int qs_lsh_prep(const uint64_t* sigs_dev, uint64_t n, uint32_t t,
+                uint64_t* keys_dev, uint32_t* tags_dev, void* stream);
+
+/* Bucket construction: per table, sort (key, id) so equal keys are contiguous
+ * with ascending ids (the stable argsort of lsh_search.py:157-164).
+ * ids_out_dev (t, n) uint32; keys_out_dev (t, n) uint64 sorted keys.
+ * Workspace bytes from qs_lsh_bucket_ws_bytes. */
+size_t qs_lsh_bucket_ws_bytes(uint64_t n, uint32_t t);
+int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t,
+                         uint64_t* keys_out_dev, uint32_t* ids_out_dev,
+                         void* ws_dev, size_t ws_bytes, void* stream);
+
+/* Bucket listing: non-singleton buckets (start position in the (t, n) sorted
+ * arrays, size) and per-table head counts.  Two calls: first with
+ * bstart_dev == NULL to count into *count_dev (uint64), then to fill. */
+size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t);
+int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t,
+                        uint64_t* bstart_dev, uint32_t* bsize_dev,
+                        uint64_t* counts_dev /* [0]=non-singleton buckets, [1]=heads */,
+                        void* ws_dev, size_t ws_bytes, void* stream);
+
+/* Search statistics from the bucket list (SearchStats, lsh_search.py:70-109):
+ * lookups_total, per-partition-table bucket sizes (histogram of sizes
+ * < hist_len into hist_dev uint64; larger sizes appended to big_dev with
+ * count in out_dev[2]), n_buckets and max bucket.  excluded_dev (n bytes)
+ * may be NULL; edges_dev holds the partition_bounds edges (p + 1 values). */
+int qs_lsh_bucket_stats(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                        const uint32_t* bsize_dev, uint64_t n_nonsingle,
+                        const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p,
+                        uint64_t* hist_dev, uint32_t hist_len, uint32_t* big_dev,
+                        uint64_t big_cap, uint64_t* out_dev /* [0]=lookups [1]=buckets-from-splits [2]=n_big [3]=max */,
+                        void* stream);
+
+/* Candidate-pair enumeration + exact collision counting + >= m threshold.
+ * Every unordered pair sharing a bucket is visited in the bucket of its
+ * FIRST colliding table only (exact dedup via bit-sliced tag comparison,
+ * verified on the 64-bit keys), so each distinct pair is counted once with
+ * sim = number of tables whose keys agree.  Applies the reference's masks
+ * (canonical c < q, q - c > excl, excluded/partition rule of
+ * lsh_search.py:256-287).  Emits (sortkey = (q - c) << 32 | c, sim) for
+ * sim >= m into out_key/out_sim (capacity cap; the true count is always
+ * written to counters_dev[1] so the caller can grow and retry);
+ * counters_dev[0] += distinct pairs.  Workspace from qs_lsh_pairs_ws_bytes. */
+size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle);
+int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                 const uint32_t* bsize_dev, uint64_t n_nonsingle,
+                 const uint64_t* keys_dev, const uint32_t* tags_dev, uint64_t n, uint32_t t,
+                 uint32_t m, uint64_t excl, const uint8_t* excluded_dev,
+                 const uint64_t* edges_dev, uint32_t p,
+                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint64_t cap,
+                 unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
+                 void* stream);
+
+/* Occurrence filter (lsh_search.py:256-274) from the matched pairs of a
+ * filter-free enumeration: per partition, degree over within-partition
+ * matched pairs, core = degree > thr * |partition|, excluded = core plus the
+ * matched within-partition neighbours of core.  excluded_dev (n bytes) is
+ * written; counters_dev[0] = number excluded.  Workspace: n * 4 bytes. */
+int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
+                             uint64_t n_pairs, uint64_t n, double threshold,
+                             const uint64_t* edges_dev, uint32_t p, uint8_t* excluded_dev,
+                             unsigned long long* counters_dev, void* ws_dev, void* stream);
+
+/* Sort matched pairs by (dt, idx1) (lsh_search.py:291) and pack them into
+ * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38).
+ * Workspace from qs_sort_pairs_ws_bytes. */
+size_t qs_sort_pairs_ws_bytes(uint64_t n);
+int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_pairs,
+                    uint32_t key_bits, uint8_t* triplets_dev, void* ws_dev, size_t ws_bytes,
+                    void* stream);
+
+/* Generic stable LSD radix sort of (uint64 key, uint32 value) pairs over
+ * `segments` independent equal-length segments, on key bits [0, key_bits). */
+size_t qs_radix_sort_ws_bytes(uint64_t seg_len, uint32_t segments);
+int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len,
+                        uint32_t segments, uint32_t key_bits, uint64_t* keys_alt_dev,
+                        uint32_t* vals_alt_dev, void* ws_dev, size_t ws_bytes,
+                        int* result_in_alt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUAKESCAN_B200_H */

@@ -1,0 +1,131 @@
+"""ctypes binding of the C ABI (include/quakescan_b200.h).
+
+The CUDA library is built in-tree (`paper_1803_09835_b200/lib/
+libquakescan_b200.so`, see csrc/Makefile / __graft_entry__.build()).  There
+is no CPU fallback: if the library is missing every hot-path call raises.
+"""
+
+import ctypes
+import os
+
+from .errors import DataError, ParameterError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libquakescan_b200.so")
+
+QS_OK, QS_ERR_ARG, QS_ERR_OOM, QS_ERR_CUDA, QS_ERR_DATA = 0, 1, 2, 3, 4
+
+_u8p = ctypes.c_void_p
+_p = ctypes.c_void_p
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+_i32 = ctypes.c_int32
+_sz = ctypes.c_size_t
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+
+# name -> (restype, argtypes); must cover every function in include/quakescan_b200.h
+SIGNATURES = {
+    "qs_version": (ctypes.c_char_p, []),
+    "qs_last_error": (ctypes.c_char_p, []),
+    "qs_device_info": (_int, [ctypes.c_char_p, _sz]),
+    "qs_gen_hash_mapping": (_int, [_p, _u32, _u32, _u64, _p]),
+    "qs_minmax_plan_bytes": (_sz, [_u32, _u32]),
+    "qs_minmax_plan": (_int, [_p, _u32, _u32, _p, _p]),
+    "qs_minmax_signatures": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p]),
+    "qs_minmax_signatures_search": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p,
+                                           _p, _p]),
+    "qs_gen_signatures_range": (_int, [_p, _u64, _u32, _p, _u32, _u32, _i32, _i32, _p, _u64,
+                                       _u64]),
+    "qs_lsh_prep": (_int, [_p, _u64, _u32, _p, _p, _p]),
+    "qs_lsh_bucket_ws_bytes": (_sz, [_u64, _u32]),
+    "qs_lsh_build_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _sz, _p]),
+    "qs_lsh_list_ws_bytes": (_sz, [_u64, _u32]),
+    "qs_lsh_list_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _sz, _p]),
+    "qs_lsh_bucket_stats": (_int, [_p, _p, _p, _u64, _p, _p, _u32, _p, _u32, _p, _u64, _p, _p]),
+    "qs_lsh_pairs_ws_bytes": (_sz, [_u64]),
+    "qs_lsh_pairs": (_int, [_p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
+                            _p, _p, _u64, _p, _p, _sz, _p]),
+    "qs_lsh_occurrence_filter": (_int, [_p, _p, _u64, _u64, _dbl, _p, _u32, _p, _p, _p, _p]),
+    "qs_sort_pairs_ws_bytes": (_sz, [_u64]),
+    "qs_lsh_finalize": (_int, [_p, _p, _u64, _u32, _p, _p, _sz, _p]),
+    "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),
+    "qs_radix_sort_pairs": (_int, [_p, _p, _u64, _u32, _u32, _p, _p, _p, _sz, _p, _p]),
+}
+
+_lib = None
+
+
+class NativeMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """The loaded library; raises NativeMissing when it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeMissing(
+                f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build() or "
+                f"make -C paper_1803_09835_b200/csrc); there is no CPU fallback")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name, None)
+            if fn is None:
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def missing_symbols():
+    handle = lib()
+    return [n for n in SIGNATURES if not hasattr(handle, n)]
+
+
+def last_error() -> str:
+    return lib().qs_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == QS_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == QS_ERR_ARG:
+        raise ParameterError(msg)
+    if rc == QS_ERR_DATA:
+        raise DataError(msg)
+    if rc == QS_ERR_OOM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)
+
+
+# ------------------------------------------------------------------ torch glue
+
+def torch():
+    import torch as _t
+    if not _t.cuda.is_available():
+        raise NativeMissing("no CUDA device: the quakescan-b200 hot path runs only on the GPU")
+    return _t
+
+
+def stream():
+    """cudaStream_t of torch's current stream (kernels are ordered with torch work)."""
+    t = torch()
+    return ctypes.c_void_p(t.cuda.current_stream().cuda_stream)
+
+
+def ptr(x):
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if x is None:
+        return None
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def is_device_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)

@@ -1,0 +1,324 @@
+// Min-Max hash signatures on sm_100a (integer ALU; no tensor-core shape).
+//
+// Reference: minmax_hash.py:73-128 (mapping, row split) and _sigcore.pyx:32-85
+// (element-major kernel: running min/max over all t*k/2 mapping columns for
+// every set bit, K*t*k/2 64-bit compare-selects per fingerprint).
+//
+// B200 design — probe MinHash: the plan stores, per hash column f, the element
+// indices in ascending mapping-value order.  For a fingerprint held as a d-bit
+// bitmap in shared memory, min_x V[x, f] is the value of the FIRST element of
+// that order present in the bitmap, and the max is the last one.  With K of d
+// bits set the expected number of probes per column is d/K (≈10 at cfg1)
+// instead of K compare-selects (400): the same outputs, bit for bit, because
+// the plan is built from the mapping values themselves (ties share a value).
+#include "qs_common.cuh"
+
+namespace qs {
+
+// -------------------------------------------------------------- mapping
+__global__ void k_gen_mapping(uint64_t* __restrict__ v, uint32_t d, uint32_t F, uint64_t seed) {
+    uint64_t total = (uint64_t)d * F;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x = i / F, j = i - x * F;
+        v[i] = fmix64(((x + 1ULL) * GOLDEN64) ^ (seed + j));
+    }
+}
+
+// ----------------------------------------------------------------- plan
+constexpr uint32_t PLAN_MAX_D = 16384;  // smem bitonic sort capacity (192 KB)
+
+static inline size_t plan_order_bytes(uint32_t d, uint32_t F) {
+    return (((size_t)d * F * sizeof(uint16_t)) + 255) & ~(size_t)255;
+}
+
+// One CTA per hash column: bitonic sort of (value, element) in shared memory,
+// then scatter into the rank-major plan (order[r * F + f], svals[r * F + f]).
+__global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, uint32_t d,
+                                               uint32_t F, uint32_t dpad,
+                                               uint16_t* __restrict__ order,
+                                               uint64_t* __restrict__ svals) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* key = (uint64_t*)smem;
+    uint32_t* idx = (uint32_t*)(key + dpad);
+    const uint32_t f = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < dpad; i += blockDim.x) {
+        if (i < d) {
+            key[i] = v[(uint64_t)i * F + f];
+            idx[i] = i;
+        } else {
+            key[i] = ~0ULL;
+            idx[i] = 0xFFFFFFFFu;
+        }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= dpad; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < dpad; i += blockDim.x) {
+                uint32_t l = i ^ j;
+                if (l > i) {
+                    bool up = (i & k) == 0;
+                    uint64_t a = key[i], b = key[l];
+                    uint32_t ia = idx[i], ib = idx[l];
+                    bool gt = (a > b) || (a == b && ia > ib);
+                    if (gt == up) {
+                        key[i] = b; key[l] = a;
+                        idx[i] = ib; idx[l] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t r = threadIdx.x; r < d; r += blockDim.x) {
+        order[(uint64_t)r * F + f] = (uint16_t)idx[r];
+        svals[(uint64_t)r * F + f] = key[r];
+    }
+}
+
+// ------------------------------------------------------------ signatures
+__device__ __forceinline__ uint64_t mix_key(uint64_t s) { return fmix64(s ^ GOLDEN64); }
+
+// One warp per fingerprint row (grid-stride).  Shared memory per warp: the
+// d-bit bitmap and the 2F probe results.
+template <bool SEARCH>
+__global__ void __launch_bounds__(256) k_signatures(
+    const uint32_t* __restrict__ bits, uint64_t n, uint32_t K,
+    const uint16_t* __restrict__ order, const uint64_t* __restrict__ svals, uint32_t d,
+    uint32_t F, uint32_t t, uint32_t kh, uint64_t* __restrict__ sigs,
+    uint64_t* __restrict__ keys, uint32_t* __restrict__ tags, uint32_t* __restrict__ bad) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t words = (d + 31) >> 5;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per_warp = ((words * 4 + 15) & ~15u) + 2 * F * 8;
+    uint32_t* bm = (uint32_t*)(smem + warp * per_warp);
+    uint64_t* vals = (uint64_t*)((unsigned char*)bm + ((words * 4 + 15) & ~15u));
+    const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t W = (t + 31) >> 5;
+    const bool vec = (K % 4 == 0) && ((((uintptr_t)bits) & 15) == 0);
+
+    for (uint64_t row = gwarp; row < n; row += nwarps) {
+        for (uint32_t w = lane; w < words; w += 32) bm[w] = 0u;
+        __syncwarp();
+        const uint32_t* rb = bits + row * K;
+        uint32_t badrow = 0;
+        if (vec) {
+            const uint4* rb4 = (const uint4*)rb;
+            for (uint32_t q = lane; q < K / 4; q += 32) {
+                uint4 x = __ldg(rb4 + q);
+                uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (xs[e] < d) atomicOr(&bm[xs[e] >> 5], 1u << (xs[e] & 31));
+                    else badrow = 1;
+                }
+            }
+        } else {
+            for (uint32_t q = lane; q < K; q += 32) {
+                uint32_t x = __ldg(rb + q);
+                if (x < d) atomicOr(&bm[x >> 5], 1u << (x & 31));
+                else badrow = 1;
+            }
+        }
+        if (__any_sync(0xffffffffu, badrow) && lane == 0) atomicExch(bad, 1u);
+        __syncwarp();
+        // merged probe loop: lane walks its columns seq = lane, lane+32, ... < 2F
+        uint32_t seq = lane, r = 0;
+        while (seq < 2 * F) {
+            const bool is_min = seq < F;
+            const uint32_t f = is_min ? seq : seq - F;
+            const uint32_t rank = is_min ? r : d - 1 - r;
+            const uint64_t pos = (uint64_t)rank * F + f;
+            const uint32_t x = __ldg(order + pos);
+            if ((bm[x >> 5] >> (x & 31)) & 1u) {
+                vals[seq] = __ldg(svals + pos);
+                seq += 32;
+                r = 0;
+            } else if (++r >= d) {  // only reachable when every bit was invalid
+                vals[seq] = 0;
+                seq += 32;
+                r = 0;
+            }
+        }
+        __syncwarp();
+        for (uint32_t wr = 0; wr < W; ++wr) {
+            const uint32_t i = wr * 32 + lane;
+            uint64_t acc = 0;
+            if (i < t) {
+                const uint64_t* mn = vals + (uint64_t)i * kh;
+                const uint64_t* mx = vals + F + (uint64_t)i * kh;
+                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mn[j]);
+                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mx[j]);
+                if (sigs) sigs[row * t + i] = acc;
+            }
+            if (SEARCH) {
+                const uint64_t key = mix_key(acc);
+                if (i < t) keys[(uint64_t)i * n + row] = key;
+                const uint32_t tag = (uint32_t)key & 0xFFFFu;
+                uint32_t plane = 0;
+#pragma unroll
+                for (int b = 0; b < 16; ++b) {
+                    uint32_t word = __ballot_sync(0xffffffffu, (i < t) && ((tag >> b) & 1u));
+                    if (lane == (uint32_t)b) plane = word;
+                }
+                if (lane < 16) tags[(row * 16 + lane) * W + wr] = plane;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+static size_t sig_smem_per_warp(uint32_t d, uint32_t F) {
+    uint32_t words = (d + 31) >> 5;
+    return ((words * 4 + 15) & ~15u) + 2 * (size_t)F * 8;
+}
+
+static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
+                             const void* plan, uint32_t d, uint32_t t, uint32_t kh,
+                             uint64_t* sigs, uint64_t* keys, uint32_t* tags, uint32_t* bad,
+                             cudaStream_t st) {
+    QS_ARG(K >= 1, "fingerprints must have at least one set bit");
+    QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
+    QS_ARG(t >= 1 && kh >= 1, "t and k/2 must be >= 1");
+    if (n == 0) return QS_OK;
+    const uint32_t F = t * kh;
+    const uint16_t* order = (const uint16_t*)plan;
+    const uint64_t* svals = (const uint64_t*)((const unsigned char*)plan + plan_order_bytes(d, F));
+    size_t per_warp = sig_smem_per_warp(d, F);
+    int warps = 8;
+    while (warps > 1 && per_warp * warps > 200 * 1024) warps >>= 1;
+    QS_ARG(per_warp <= 220 * 1024, "t*k too large for the signature kernel (F=%u)", F);
+    size_t smem = per_warp * warps;
+    unsigned threads = warps * 32;
+    uint64_t want = (n + warps - 1) / warps;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (search) {
+        QS_CUDA(cudaFuncSetAttribute(k_signatures<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signatures<true>, threads, smem);
+    } else {
+        QS_CUDA(cudaFuncSetAttribute(k_signatures<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_signatures<false>, threads, smem);
+    }
+    if (per_sm < 1) per_sm = 1;
+    uint64_t cap = (uint64_t)sms * per_sm * 4;
+    unsigned grid = (unsigned)(want < cap ? want : cap);
+    if (search)
+        k_signatures<true><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
+                                                         sigs, keys, tags, bad);
+    else
+        k_signatures<false><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
+                                                          sigs, nullptr, nullptr, bad);
+    QS_CHECK_LAUNCH("k_signatures");
+    return QS_OK;
+}
+
+}  // namespace qs
+
+using namespace qs;
+
+extern "C" {
+
+int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs, uint64_t seed,
+                        void* stream) {
+    QS_ARG(d >= 1 && n_funcs >= 1, "d and n_funcs must be >= 1");
+    uint64_t total = (uint64_t)d * n_funcs;
+    k_gen_mapping<<<qs_blocks(total, 256), 256, 0, (cudaStream_t)stream>>>(values_dev, d, n_funcs, seed);
+    QS_CHECK_LAUNCH("k_gen_mapping");
+    return QS_OK;
+}
+
+size_t qs_minmax_plan_bytes(uint32_t d, uint32_t n_funcs) {
+    return plan_order_bytes(d, n_funcs) + (size_t)d * n_funcs * sizeof(uint64_t);
+}
+
+int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs, void* plan_dev,
+                   void* stream) {
+    QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
+    QS_ARG(n_funcs >= 1, "n_funcs must be >= 1");
+    uint32_t dpad = 1;
+    while (dpad < d) dpad <<= 1;
+    if (dpad < 2) dpad = 2;
+    size_t smem = (size_t)dpad * (sizeof(uint64_t) + sizeof(uint32_t));
+    QS_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "smem attr");
+    uint16_t* order = (uint16_t*)plan_dev;
+    uint64_t* svals = (uint64_t*)((unsigned char*)plan_dev + plan_order_bytes(d, n_funcs));
+    unsigned threads = dpad >= 1024 ? 1024 : dpad;
+    k_plan<<<n_funcs, threads, smem, (cudaStream_t)stream>>>(values_dev, d, n_funcs, dpad, order, svals);
+    QS_CHECK_LAUNCH("k_plan");
+    return QS_OK;
+}
+
+int qs_minmax_signatures(const uint32_t* bits_dev, uint64_t n, uint32_t K, const void* plan_dev,
+                         uint32_t d, uint32_t t, uint32_t k_half, uint64_t* out_dev,
+                         uint32_t* bad_dev, void* stream) {
+    return launch_signatures(false, bits_dev, n, K, plan_dev, d, t, k_half, out_dev, nullptr,
+                             nullptr, bad_dev, (cudaStream_t)stream);
+}
+
+int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K,
+                                const void* plan_dev, uint32_t d, uint32_t t, uint32_t k_half,
+                                uint64_t* sigs_dev, uint64_t* keys_dev, uint32_t* tags_dev,
+                                uint32_t* bad_dev, void* stream) {
+    return launch_signatures(true, bits_dev, n, K, plan_dev, d, t, k_half, sigs_dev, keys_dev,
+                             tags_dev, bad_dev, (cudaStream_t)stream);
+}
+
+int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
+                            const uint64_t* values, uint32_t d, uint32_t F, int32_t t,
+                            int32_t k_half, uint64_t* out, uint64_t start, uint64_t stop) {
+    QS_ARG(t >= 1 && k_half >= 1 && (uint64_t)t * (uint64_t)k_half == F,
+           "mapping width does not match t * k_half");
+    QS_ARG(K >= 1, "fingerprints must have at least one set bit");
+    QS_ARG(start <= stop && stop <= n_rows, "row range out of bounds");
+    if (stop == start) return QS_OK;
+    cudaStream_t st;
+    QS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    const uint64_t rows = stop - start;
+    const uint64_t chunk = rows < (1u << 20) ? rows : (1u << 20);
+    uint64_t *dv = nullptr, *dout = nullptr;
+    uint32_t *dbits = nullptr, *dbad = nullptr;
+    void* plan = nullptr;
+    int rc = QS_OK;
+    cudaError_t e = cudaSuccess;
+    size_t pb = qs_minmax_plan_bytes(d, F);
+    if ((e = cudaMallocAsync((void**)&dv, (size_t)d * F * 8, st)) != cudaSuccess ||
+        (e = cudaMallocAsync(&plan, pb, st)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&dbits, chunk * K * 4, st)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&dout, chunk * (uint64_t)t * 8, st)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&dbad, 4, st)) != cudaSuccess) {
+        rc = cuda_status(e, "cudaMallocAsync");
+    }
+    if (rc == QS_OK) {
+        cudaMemcpyAsync(dv, values, (size_t)d * F * 8, cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(dbad, 0, 4, st);
+        rc = qs_minmax_plan(dv, d, F, plan, st);
+    }
+    for (uint64_t a = start; rc == QS_OK && a < stop; a += chunk) {
+        uint64_t m = (stop - a) < chunk ? (stop - a) : chunk;
+        cudaMemcpyAsync(dbits, bits + a * K, m * K * 4, cudaMemcpyHostToDevice, st);
+        rc = qs_minmax_signatures(dbits, m, K, plan, d, (uint32_t)t, (uint32_t)k_half, dout, dbad, st);
+        if (rc == QS_OK)
+            cudaMemcpyAsync(out + a * t, dout, m * (uint64_t)t * 8, cudaMemcpyDeviceToHost, st);
+    }
+    uint32_t hbad = 0;
+    if (rc == QS_OK) cudaMemcpyAsync(&hbad, dbad, 4, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dv, st);
+    cudaFreeAsync(plan, st);
+    cudaFreeAsync(dbits, st);
+    cudaFreeAsync(dout, st);
+    cudaFreeAsync(dbad, st);
+    e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc == QS_OK && e != cudaSuccess) rc = cuda_status(e, "qs_gen_signatures_range");
+    if (rc == QS_OK && hbad) {
+        set_error("fingerprint bit index out of range for mapping");
+        rc = QS_ERR_DATA;
+    }
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// Stable LSD radix sort of (uint64 key, uint32 value) pairs, batched over
+// equal-length independent segments (one segment per LSH table).
+//
+// Per 8-bit digit pass: (1) per-tile digit histograms, (2) per-segment
+// exclusive scan over (digit, tile), (3) stable scatter: each tile ranks its
+// keys per digit in input order (warp match_any + per-warp counters, then a
+// cross-warp prefix), so equal digits keep their relative order.
+#include "qs_common.cuh"
+
+namespace qs {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per tile
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_RADIX = 256;
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys,
+                                                        uint64_t seg_len, uint32_t tiles,
+                                                        uint32_t shift,
+                                                        uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[RS_RADIX];
+    const uint32_t tile = blockIdx.x, seg = blockIdx.y;
+    for (int i = threadIdx.x; i < RS_RADIX; i += RS_THREADS) h[i] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)seg * seg_len;
+    const uint64_t lo = (uint64_t)tile * RS_TILE;
+    const uint64_t hi = min(seg_len, lo + RS_TILE);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += RS_THREADS)
+        atomicAdd(&h[(keys[base + i] >> shift) & 0xFF], 1u);
+    __syncthreads();
+    for (int dgt = threadIdx.x; dgt < RS_RADIX; dgt += RS_THREADS)
+        hist[((uint64_t)seg * RS_RADIX + dgt) * tiles + tile] = h[dgt];
+}
+
+// One CTA per segment: exclusive scan (in place) of RS_RADIX * tiles counts.
+__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* __restrict__ hist, uint64_t len) {
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    uint32_t* a = hist + (uint64_t)blockIdx.x * len;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t b0 = 0; b0 < len; b0 += 1024 * 4) {
+        uint32_t v[4], s = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            uint64_t i = b0 + threadIdx.x * 4 + e;
+            v[e] = i < len ? a[i] : 0;
+            s += v[e];
+        }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= (uint32_t)o) w += y;
+            }
+            warp_sums[lane] = w;
+        }
+        __syncthreads();
+        uint32_t excl = carry + (warp ? warp_sums[warp - 1] : 0) + x - s;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            uint64_t i = b0 + threadIdx.x * 4 + e;
+            if (i < len) a[i] = excl;
+            excl += v[e];
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
+    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t seg_len,
+    uint32_t tiles, uint32_t shift, const uint32_t* __restrict__ offs,
+    uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals) {
+    __shared__ uint32_t wcnt[RS_WARPS][RS_RADIX];
+    __shared__ uint32_t toff[RS_RADIX];
+    const uint32_t tile = blockIdx.x, seg = blockIdx.y;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < RS_WARPS * RS_RADIX; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+    for (int dgt = threadIdx.x; dgt < RS_RADIX; dgt += RS_THREADS)
+        toff[dgt] = offs[((uint64_t)seg * RS_RADIX + dgt) * tiles + tile];
+    __syncthreads();
+    const uint64_t base = (uint64_t)seg * seg_len;
+    const uint64_t t0 = (uint64_t)tile * RS_TILE + (uint64_t)warp * (32 * RS_ITEMS);
+    uint64_t k[RS_ITEMS];
+    uint32_t v[RS_ITEMS];
+    uint32_t rank[RS_ITEMS];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint64_t i = t0 + (uint64_t)r * 32 + lane;
+        const bool ok = i < seg_len;
+        k[r] = ok ? keys[base + i] : 0;
+        v[r] = ok ? vals[base + i] : 0;
+        const uint32_t dgt = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : 0x100u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dgt);
+        const uint32_t cnt = __popc(peers);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t b = 0;
+        if (ok) b = wcnt[warp][dgt];
+        rank[r] = b + before;
+        __syncwarp();
+        if (ok && before == 0) wcnt[warp][dgt] = b + cnt;
+        __syncwarp();
+    }
+    __syncthreads();
+    // exclusive prefix across warps per digit
+    for (int dgt = threadIdx.x; dgt < RS_RADIX; dgt += RS_THREADS) {
+        uint32_t run = toff[dgt];
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) {
+            uint32_t c = wcnt[w][dgt];
+            wcnt[w][dgt] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint64_t i = t0 + (uint64_t)r * 32 + lane;
+        if (i < seg_len) {
+            const uint32_t dgt = (uint32_t)((k[r] >> shift) & 0xFF);
+            const uint64_t pos = base + wcnt[warp][dgt] + rank[r];
+            okeys[pos] = k[r];
+            ovals[pos] = v[r];
+        }
+    }
+}
+
+static uint32_t rs_tiles(uint64_t seg_len) { return (uint32_t)((seg_len + RS_TILE - 1) / RS_TILE); }
+
+size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments) {
+    return (size_t)rs_tiles(seg_len) * RS_RADIX * segments * sizeof(uint32_t) + 256;
+}
+
+int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
+                     uint32_t key_bits, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
+                     size_t ws_bytes, int* in_alt, cudaStream_t st) {
+    *in_alt = 0;
+    if (seg_len == 0 || segments == 0 || key_bits == 0) return QS_OK;
+    QS_ARG(seg_len < (1ull << 32), "radix sort segment longer than 2^32");
+    QS_ARG(ws_bytes >= radix_ws_bytes(seg_len, segments), "radix sort workspace too small");
+    const uint32_t tiles = rs_tiles(seg_len);
+    QS_ARG(tiles <= 65535u * 64u, "too many tiles");
+    uint32_t* hist = (uint32_t*)ws;
+    uint64_t *src_k = keys, *dst_k = keys_alt;
+    uint32_t *src_v = vals, *dst_v = vals_alt;
+    for (uint32_t shift = 0; shift < key_bits; shift += 8) {
+        dim3 grid(tiles, segments);
+        k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
+        k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
+        k_rs_scatter<<<grid, RS_THREADS, 0, st>>>(src_k, src_v, seg_len, tiles, shift, hist,
+                                                  dst_k, dst_v);
+        QS_CHECK_LAUNCH("radix sort pass");
+        uint64_t* tk = src_k; src_k = dst_k; dst_k = tk;
+        uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
+        *in_alt ^= 1;
+    }
+    return QS_OK;
+}
+
+}  // namespace qs
+
+extern "C" {
+
+size_t qs_radix_sort_ws_bytes(uint64_t seg_len, uint32_t segments) {
+    return qs::radix_ws_bytes(seg_len, segments);
+}
+
+int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len,
+                        uint32_t segments, uint32_t key_bits, uint64_t* keys_alt_dev,
+                        uint32_t* vals_alt_dev, void* ws_dev, size_t ws_bytes,
+                        int* result_in_alt, void* stream) {
+    QS_ARG(key_bits <= 64, "key_bits must be <= 64");
+    return qs::radix_sort_pairs(keys_dev, vals_dev, seg_len, segments, key_bits, keys_alt_dev,
+                                vals_alt_dev, ws_dev, ws_bytes, result_in_alt,
+                                (cudaStream_t)stream);
+}
+
+}  // extern "C"

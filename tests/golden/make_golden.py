@@ -1,0 +1,200 @@
+"""Generate tests/golden/* by running the REFERENCE implementation.
+
+Runs only in the build container, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+It imports the reference package `quakescan` from /root/reference/pkg/src
+(the reference's compiled `_sigcore`, built into oracle/_ref by
+`make -C oracle ref`, is registered as `quakescan._sigcore` when present;
+otherwise the reference's own bit-identical numpy backend is used) and records
+inputs and outputs of the hot-path functions as small fixtures. Nothing on
+the GPU box reads /root/reference; the fixtures travel instead.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import oracle  # noqa: E402
+
+core = oracle.ref_sigcore()
+if core is not None:
+    sys.modules["quakescan._sigcore"] = core
+
+from quakescan import fingerprint as rfp  # noqa: E402
+from quakescan import lsh_search as rls  # noqa: E402
+from quakescan import minmax_hash as rmh  # noqa: E402
+from quakescan.ingest import TimeSeries  # noqa: E402
+
+from paper_1803_09835_b200 import workloads  # noqa: E402
+
+
+def kat():
+    xs = [0, 1, 2, 0xDEADBEEF, 2**63, 2**64 - 1, 0x0123456789ABCDEF, 12345]
+    fm = {hex(x): hex(int(rmh.fmix64(np.array([x], np.uint64))[0])) for x in xs}
+    hv = {}
+    for x, s in [(0, 0), (1, 0), (0, 1), (12345, 67890), (8191, 2**63), (4095, 2**64 - 1)]:
+        hv[f"{x},{s}"] = hex(int(rmh.hash_values(np.array([x], np.uint64), s)[0]))
+    cb = {}
+    for ws in [(0,), (1, 2), (5, 9, 3), (2**64 - 1, 0, 7, 2**63)]:
+        cb[",".join(str(w) for w in ws)] = hex(rmh.combine(np.array(ws, np.uint64)))
+    m = rmh.gen_hash_mapping(d=64, t=3, k=4, seed=42)
+    sig = rmh.signatures(np.array([[0, 5, 17, 63]], np.uint32), m)[0]
+    return dict(fmix64=fm, hash=hv, combine=cb,
+                sig_d64_t3_k4_s42_bits_0_5_17_63=[hex(int(v)) for v in sig],
+                backend=rmh.BACKEND)
+
+
+def minmax_cases():
+    rng = np.random.default_rng(31)
+    cases = {}
+    for name, (n, d, K, t, k, seed) in {
+        "small": (64, 1024, 50, 10, 6, 3),
+        "cfg0shape": (256, 4096, 200, 100, 4, 0),
+        "cfg1shape": (512, 4096, 400, 100, 4, 0),
+        "odd": (33, 97, 7, 5, 2, 2**64 - 3),
+        "k8": (40, 8192, 100, 13, 8, 12345),
+    }.items():
+        bits = np.stack([np.sort(rng.choice(d, K, replace=False)) for _ in range(n)]).astype(np.uint32)
+        m = rmh.gen_hash_mapping(d, t, k, seed)
+        sigs = rmh.signatures(bits, m)
+        cases[name] = dict(bits=bits, sigs=sigs, meta=np.array([d, t, k], np.int64),
+                           seed=np.array([seed], np.uint64))
+    return cases
+
+
+def search_case(sigs, **cfg):
+    excl = cfg.pop("exclusion_windows", 0)
+    rec, st = rls.search_signatures(sigs, rls.SearchConfig(**cfg), exclusion_windows=excl)
+    return rec, st.to_dict()
+
+
+def burst_corpus(rng, n=400, burst=60, k_bits=60, d=2048):
+    bits = np.stack([np.sort(rng.choice(d, k_bits, replace=False)) for _ in range(n)]).astype(np.uint32)
+    rows = rng.permutation(n)
+    burst_rows = np.sort(rows[:burst])
+    pair_rows = np.sort(rows[burst:burst + 2])
+    template = np.sort(rng.choice(d, k_bits, replace=False))
+    pool = np.setdiff1d(np.arange(d), template)
+    for r in burst_rows:
+        churn = rng.integers(0, 4)
+        keep = rng.choice(k_bits, k_bits - churn, replace=False)
+        bits[r] = np.sort(np.concatenate([template[keep], rng.choice(pool, churn, replace=False)]))
+    event = np.sort(rng.choice(d, k_bits, replace=False))
+    bits[pair_rows[0]] = event
+    bits[pair_rows[1]] = event
+    return bits
+
+
+def search_cases():
+    rng = np.random.default_rng(5)
+    out = {}
+    prone = rng.integers(0, 40, size=(300, 16)).astype(np.uint64)
+    for p in (1, 2, 3, 8):
+        out[f"prone_p{p}"] = (prone, dict(tables=16, hash_funcs=2, min_matches=3,
+                                          partitions=p, exclusion_windows=2))
+    tiny = rng.integers(0, 5, size=(150, 10)).astype(np.uint64)
+    out["tiny_alpha_excl0"] = (tiny, dict(tables=10, hash_funcs=2, min_matches=2))
+    out["tiny_alpha_excl5_p3"] = (tiny, dict(tables=10, hash_funcs=2, min_matches=2,
+                                             partitions=3, exclusion_windows=5))
+    out["tiny_alpha_occ"] = (tiny, dict(tables=10, hash_funcs=2, min_matches=2,
+                                        occurrence_threshold=0.2, exclusion_windows=1))
+    out["tiny_alpha_occ_p4"] = (tiny, dict(tables=10, hash_funcs=2, min_matches=2,
+                                           occurrence_threshold=0.2, partitions=4))
+    bits = burst_corpus(np.random.default_rng(9))
+    m = rmh.gen_hash_mapping(2048, 32, 4, 1)
+    bs = rmh.signatures(bits, m)
+    out["burst_off"] = (bs, dict(tables=32, hash_funcs=4, min_matches=2))
+    out["burst_on"] = (bs, dict(tables=32, hash_funcs=4, min_matches=2, occurrence_threshold=0.05))
+    out["burst_on_p4"] = (bs, dict(tables=32, hash_funcs=4, min_matches=2,
+                                   occurrence_threshold=0.05, partitions=4))
+    out["empty"] = (np.zeros((0, 4), np.uint64), dict(tables=4, hash_funcs=2, min_matches=1))
+    out["single"] = (np.zeros((1, 4), np.uint64), dict(tables=4, hash_funcs=2, min_matches=1))
+    out["all_same"] = (np.full((64, 6), 7, np.uint64), dict(tables=6, hash_funcs=2, min_matches=6,
+                                                           exclusion_windows=3))
+    out["all_same_occ"] = (np.full((64, 6), 7, np.uint64),
+                           dict(tables=6, hash_funcs=2, min_matches=6, occurrence_threshold=0.5,
+                                partitions=2))
+    # cfg1-shaped: 400-of-4096, t=100, k=4, m=5, planted pairs and noise groups
+    cbits, _ = workloads.cfg1_bits(n=3000, seed=11, pair_frac=1 / 60, group_frac=1 / 1000)
+    cm = rmh.gen_hash_mapping(4096, 100, 4, 0)
+    csig = rmh.signatures(cbits, cm)
+    out["cfg1_small"] = (csig, dict(tables=100, hash_funcs=4, min_matches=5))
+    out["cfg1_small_occ"] = (csig, dict(tables=100, hash_funcs=4, min_matches=5,
+                                        occurrence_threshold=120 / 3000))
+    out["cfg1_small_occ_p3"] = (csig, dict(tables=100, hash_funcs=4, min_matches=5,
+                                           occurrence_threshold=60 / 3000, partitions=3,
+                                           exclusion_windows=7))
+    res = {}
+    for name, (sigs, cfg) in out.items():
+        rec, st = search_case(sigs, **dict(cfg))
+        res[name] = (sigs, cfg, rec, st)
+    return res
+
+
+def fingerprint_cases():
+    cases = {}
+    x, _ = workloads.cfg0_trace(n_samples=60 * 60 * 100 // 2, seed=3, copies=4)
+    p = workloads.CFG0_PARAMS
+    params = rfp.FingerprintParams(
+        window_len_s=p["window_len_s"], window_lag_s=p["window_lag_s"],
+        freq_bins=p["freq_bins"], time_bins=p["time_bins"], top_k=p["top_k"],
+        band_low_hz=p["band_low_hz"], band_high_hz=p["band_high_hz"],
+        stft=rfp.StftParams(frame_len_s=p["frame_len_s"], hop_s=p["hop_s"]))
+    ts = TimeSeries("ST0", "HHZ", 100.0, 1000.0, x)
+    fps, mad = rfp.fingerprint_series(ts, params, mad_rate=0.1, mad_seed=0)
+    freqs, times, logpow = rfp.spectrogram(ts, params)
+    r0, r1 = rfp._band_rows(freqs, params)
+    sel = np.array([0, 1, 7, 100, 555, fps.bits.shape[0] - 1])
+    _, _, coeffs = next(rfp.iter_coeff_batches(ts, params, indices=sel))
+    _, _, imgs = next(rfp.iter_image_batches(ts, params, indices=sel))
+    cases["cfg0_half_hour"] = dict(
+        samples=x, bits=fps.bits, median=mad.median, mad=mad.mad,
+        band=np.ascontiguousarray(logpow[r0:r1].T), band_rows=np.array([r0, r1]),
+        sel=sel, coeffs=coeffs, images=imgs,
+        meta=np.array([mad.n_sampled, mad.n_total]))
+    # small reference-test geometry with a non-power-of-two image side
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal(30_000).astype(np.float32)
+    small = rfp.FingerprintParams(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=12,
+                                  top_k=24, stft=rfp.StftParams(frame_len_s=0.5, hop_s=0.05))
+    ts2 = TimeSeries("ST1", "HHZ", 100.0, 0.0, y)
+    fps2, mad2 = rfp.fingerprint_series(ts2, small, mad_rate=1.0)
+    cases["small_full_band"] = dict(samples=y, bits=fps2.bits, median=mad2.median, mad=mad2.mad,
+                                    meta=np.array([mad2.n_sampled, mad2.n_total]))
+    return cases
+
+
+def main():
+    with open(os.path.join(HERE, "kat.json"), "w") as f:
+        json.dump(kat(), f, indent=1, sort_keys=True)
+    mm = minmax_cases()
+    np.savez_compressed(os.path.join(HERE, "minmax.npz"),
+                        **{f"{c}__{k}": v for c, d in mm.items() for k, v in d.items()})
+    sc = search_cases()
+    arrays, meta, seen = {}, {}, {}
+    for name, (sigs, cfg, rec, st) in sc.items():
+        key = seen.setdefault(id(sigs), f"sigs{len(seen)}")
+        arrays[key] = sigs
+        arrays[f"{name}__trip"] = rec
+        meta[name] = dict(cfg=cfg, stats=st, sigs=key)
+    np.savez_compressed(os.path.join(HERE, "search.npz"), **arrays)
+    with open(os.path.join(HERE, "search.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    fc = fingerprint_cases()
+    np.savez_compressed(os.path.join(HERE, "fingerprint.npz"),
+                        **{f"{c}__{k}": v for c, d in fc.items() for k, v in d.items()})
+    for fn in sorted(os.listdir(HERE)):
+        print(fn, os.path.getsize(os.path.join(HERE, fn)))
+
+
+if __name__ == "__main__":
+    main()
