@@ -1,0 +1,425 @@
+"""LSH similarity search on the B200 — drop-in for reference lsh_search.py.
+
+Public surface of the reference module (lsh_search.py:35-333): TRIPLET_DTYPE,
+PROFILES, SearchConfig, SearchStats, detection_probability, partition_bounds,
+search_signatures, exclusion_windows_for, search_fingerprints.  Results are
+identical to the reference's: triplets (dt, idx1, sim) sorted by (dt, idx1),
+the same occurrence-filter decisions (including the order-dependent
+per-partition exclusion semantics of lsh_search.py:244-287) and the same
+SearchStats fields.
+
+Every stage runs in sm_100a kernels through the C ABI (csrc/qs_lsh.cu,
+csrc/qs_sort.cu); this module only validates, allocates device buffers
+(torch's caching allocator) and sequences the launches.
+"""
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConsistencyError, ParameterError
+from .minmax_hash import HashMapping, gen_hash_mapping
+
+TRIPLET_DTYPE = np.dtype([("dt", "<u8"), ("idx1", "<u8"), ("sim", "<u4")])
+
+# (hash_funcs, min_matches) presets (lsh_search.py:40-42)
+PROFILES = {"baseline": (6, 5), "optimized": (8, 2)}
+
+_HIST_LEN = 1 << 16
+_cap_hint = {}
+
+
+@dataclass
+class SearchConfig:
+    tables: int = 100
+    hash_funcs: int = 6
+    min_matches: int = 5
+    seed: int = 0
+    partitions: int = 1
+    near_repeat_exclusion_s: float | None = None  # None -> window length
+    occurrence_threshold: float | None = None
+
+    def validate(self) -> None:
+        if self.tables < 1:
+            raise ParameterError("tables must be >= 1")
+        if self.hash_funcs < 2 or self.hash_funcs % 2:
+            raise ParameterError("hash_funcs must be a positive even number")
+        if not 1 <= self.min_matches <= self.tables:
+            raise ParameterError("min_matches must be in [1, tables]")
+        if self.partitions < 1:
+            raise ParameterError("partitions must be >= 1")
+        if self.occurrence_threshold is not None and not 0 < self.occurrence_threshold <= 1:
+            raise ParameterError("occurrence_threshold must be in (0, 1]")
+        if self.near_repeat_exclusion_s is not None and self.near_repeat_exclusion_s < 0:
+            raise ParameterError("near_repeat_exclusion_s must be >= 0")
+
+
+@dataclass
+class SearchStats:
+    n_fingerprints: int = 0
+    n_queries: int = 0
+    partitions: list = field(default_factory=list)
+    lookups_total: int = 0
+    distinct_pairs: int = 0
+    emitted_triplets: int = 0
+    filtered_fingerprints: int = 0
+    peak_table_entries: int = 0
+    n_buckets: int = 0
+    top_bucket_mass: float = 0.0  # share of entries in the largest 0.1% buckets
+    max_bucket: int = 0
+
+    @property
+    def lookups_per_query(self) -> float:
+        return self.lookups_total / self.n_queries if self.n_queries else 0.0
+
+    @property
+    def selectivity(self) -> float:
+        """Mean fraction of the dataset compared per query."""
+        n = self.n_fingerprints
+        return 2.0 * self.distinct_pairs / (n * n) if n else 0.0
+
+    def to_dict(self) -> dict:
+        return {
+            "n_fingerprints": self.n_fingerprints,
+            "n_queries": self.n_queries,
+            "partitions": [[int(a), int(b)] for a, b in self.partitions],
+            "lookups_total": int(self.lookups_total),
+            "lookups_per_query": self.lookups_per_query,
+            "distinct_pairs": int(self.distinct_pairs),
+            "selectivity": self.selectivity,
+            "emitted_triplets": int(self.emitted_triplets),
+            "filtered_fingerprints": int(self.filtered_fingerprints),
+            "peak_table_entries": int(self.peak_table_entries),
+            "n_buckets": int(self.n_buckets),
+            "top_bucket_mass": self.top_bucket_mass,
+            "max_bucket": int(self.max_bucket),
+        }
+
+
+def detection_probability(s: float, k: int, m: int, t: int) -> float:
+    """P(a pair with Jaccard s matches in >= m of t tables), p = s**k
+    (lsh_search.py:112-136; scalar host math, not a hot path)."""
+    if not 0.0 <= s <= 1.0:
+        raise ParameterError("similarity must be in [0, 1]")
+    if k < 1 or t < 1 or not 1 <= m <= t:
+        raise ParameterError("need k >= 1 and 1 <= m <= t")
+    p = s ** k
+    if p <= 0.0:
+        return 0.0
+    if p >= 1.0:
+        return 1.0
+    log_p = k * math.log(s)
+    log_q = math.log1p(-p)
+    lg_t = math.lgamma(t + 1)
+    terms = [lg_t - math.lgamma(i + 1) - math.lgamma(t - i + 1) + i * log_p + (t - i) * log_q
+             for i in range(m, t + 1)]
+    top = max(terms)
+    return min(1.0, math.exp(top) * sum(math.exp(x - top) for x in terms))
+
+
+def partition_bounds(n: int, partitions: int) -> list[tuple[int, int]]:
+    """Split [0, n) into near-even contiguous index ranges (lsh_search.py:139-144)."""
+    if partitions < 1:
+        raise ParameterError("partitions must be >= 1")
+    edges = np.linspace(0, n, min(partitions, max(1, n)) + 1, dtype=int)
+    return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+def exclusion_windows_for(fps, cfg: SearchConfig) -> int:
+    """Near-repeat suppression radius in window-index units (lsh_search.py:306-311)."""
+    excl_s = cfg.near_repeat_exclusion_s
+    if excl_s is None:
+        excl_s = fps.window_len_s
+    return int(math.ceil(excl_s / fps.window_lag_s)) if excl_s > 0 else 0
+
+
+# ---------------------------------------------------------------- device path
+
+class DeviceSearch:
+    """Device buffers + launches of one search over table-major keys/tags.
+
+    keys: (t, n) int64 CUDA tensor (mix64 of the signature words);
+    tags: (n, 16, ceil(t/32)) int32 CUDA tensor.  Also records per-stage CUDA
+    event times when `timing` is set (used by bench.py)."""
+
+    def __init__(self, keys, tags, n: int, t: int, timing: bool = False):
+        self.torch = nat.torch()
+        self.keys, self.tags, self.n, self.t = keys, tags, n, t
+        self.timing = timing
+        self.events = []
+        self.launches = 0
+
+    def _mark(self, name):
+        if self.timing:
+            ev = self.torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.events.append((name, ev))
+
+    def stage_times_ms(self):
+        out = {}
+        for (a, ea), (_, eb) in zip(self.events[:-1], self.events[1:]):
+            out[a] = out.get(a, 0.0) + ea.elapsed_time(eb)
+        return out
+
+    def buckets(self):
+        torch, n, t = self.torch, self.n, self.t
+        lib = nat.lib()
+        self._mark("buckets")
+        self.skeys = torch.empty((t, n), dtype=torch.int64, device=self.keys.device)
+        self.sids = torch.empty((t, n), dtype=torch.int32, device=self.keys.device)
+        ws = torch.empty(int(lib.qs_lsh_bucket_ws_bytes(n, t)), dtype=torch.uint8, device=self.keys.device)
+        nat.call("qs_lsh_build_buckets", nat.ptr(self.keys), n, t, nat.ptr(self.skeys),
+                 nat.ptr(self.sids), nat.ptr(ws), ws.numel(), nat.stream())
+        del ws
+        self.launches += 2 + 3 * 8
+        self._mark("list")
+        lws = torch.empty(int(lib.qs_lsh_list_ws_bytes(n, t)), dtype=torch.uint8, device=self.keys.device)
+        counts = torch.zeros(2, dtype=torch.int64, device=self.keys.device)
+        nat.call("qs_lsh_list_buckets", nat.ptr(self.skeys), n, t, None, None, nat.ptr(counts),
+                 nat.ptr(lws), lws.numel(), nat.stream())
+        nb, heads = (int(v) for v in counts.tolist())
+        self.nb, self.heads = nb, heads
+        self.bstart = torch.empty(max(nb, 1), dtype=torch.int64, device=self.keys.device)
+        self.bsize = torch.empty(max(nb, 1), dtype=torch.int32, device=self.keys.device)
+        if nb:
+            nat.call("qs_lsh_list_buckets", nat.ptr(self.skeys), n, t, nat.ptr(self.bstart),
+                     nat.ptr(self.bsize), nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
+        self.launches += 4 + 7
+        del self.skeys  # only ids and bucket list are needed downstream
+
+    def pairs(self, m, excl, emask, edges, p, cap=None):
+        """Enumerate; returns (pair_key int64, pair_sim int32, n_matched, distinct)."""
+        torch, lib = self.torch, nat.lib()
+        self._mark("pairs")
+        key = ("cap", self.n, self.t)
+        if cap is None:
+            cap = max(1 << 16, _cap_hint.get(key, 4 * self.n))
+        counters = torch.zeros(2, dtype=torch.int64, device=self.keys.device)
+        ws = torch.empty(int(lib.qs_lsh_pairs_ws_bytes(self.nb)), dtype=torch.uint8, device=self.keys.device)
+        while True:
+            pk = torch.empty(cap, dtype=torch.int64, device=self.keys.device)
+            ps = torch.empty(cap, dtype=torch.int32, device=self.keys.device)
+            counters.zero_()
+            nat.call("qs_lsh_pairs", nat.ptr(self.sids), nat.ptr(self.bstart), nat.ptr(self.bsize),
+                     self.nb, nat.ptr(self.keys), nat.ptr(self.tags), self.n, self.t, m, excl,
+                     nat.ptr(emask), nat.ptr(edges), p, nat.ptr(pk), nat.ptr(ps), cap,
+                     nat.ptr(counters), nat.ptr(ws), ws.numel(), nat.stream())
+            self.launches += 3
+            distinct, matched = (int(v) for v in counters.tolist())
+            if matched <= cap:
+                break
+            cap = int(matched * 1.1) + 1024
+            _cap_hint[key] = cap
+        _cap_hint[key] = max(_cap_hint.get(key, 0), int(matched * 1.1) + 1024)
+        return pk[:matched], ps[:matched], matched, distinct
+
+    def occurrence(self, pk, ps, matched, threshold, edges, p):
+        torch = self.torch
+        self._mark("filter")
+        emask = torch.empty(self.n, dtype=torch.uint8, device=self.keys.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.keys.device)
+        ws = torch.empty(self.n, dtype=torch.int32, device=self.keys.device)
+        nat.call("qs_lsh_occurrence_filter", nat.ptr(pk), nat.ptr(ps), matched, self.n,
+                 float(threshold), nat.ptr(edges), p, nat.ptr(emask), nat.ptr(cnt), nat.ptr(ws),
+                 nat.stream())
+        self.launches += 4
+        return emask, int(cnt.item())
+
+    def bucket_stats(self, emask, edges, p):
+        torch = self.torch
+        self._mark("stats")
+        hist = torch.zeros(_HIST_LEN, dtype=torch.int64, device=self.keys.device)
+        big_cap = max(1024, self.nb // 64)
+        big = torch.empty(big_cap, dtype=torch.int32, device=self.keys.device)
+        out = torch.zeros(4, dtype=torch.int64, device=self.keys.device)
+        nat.call("qs_lsh_bucket_stats", nat.ptr(self.sids), nat.ptr(self.bstart), nat.ptr(self.bsize),
+                 self.nb, nat.ptr(emask), nat.ptr(edges), p, nat.ptr(hist), _HIST_LEN, nat.ptr(big),
+                 big_cap, nat.ptr(out), nat.stream())
+        self.launches += 1
+        looks, pieces, n_big, mx = (int(v) for v in out.tolist())
+        if n_big > big_cap:
+            raise RuntimeError("bucket size overflow list too small")
+        return looks, pieces, mx, hist.cpu().numpy(), big[:n_big].cpu().numpy()
+
+    def finalize(self, pk, ps, matched):
+        torch, lib = self.torch, nat.lib()
+        self._mark("sort")
+        trip = torch.empty(matched * 20, dtype=torch.uint8, device=self.keys.device)
+        if matched:
+            ws = torch.empty(int(lib.qs_sort_pairs_ws_bytes(matched)), dtype=torch.uint8,
+                             device=self.keys.device)
+            key_bits = 32 + max(1, int(self.n).bit_length())
+            nat.call("qs_lsh_finalize", nat.ptr(pk), nat.ptr(ps), matched, key_bits,
+                     nat.ptr(trip), nat.ptr(ws), ws.numel(), nat.stream())
+            self.launches += 3 * ((key_bits + 7) // 8) + 1
+        self._mark("end")
+        return trip
+
+
+def _top_mass(hist, big, n_buckets, total):
+    top = max(1, int(math.ceil(0.001 * n_buckets)))
+    need, acc = top, 0
+    for v in sorted(big.tolist(), reverse=True):
+        if need == 0:
+            break
+        acc += v
+        need -= 1
+    idx = np.flatnonzero(hist)[::-1]
+    for s in idx:
+        if need == 0:
+            break
+        take = min(need, int(hist[s]))
+        acc += take * int(s)
+        need -= take
+    return float(acc / total) if total else 0.0
+
+
+def run_search(keys, tags, n: int, t: int, cfg: SearchConfig, exclusion_windows: int,
+               timing: bool = False):
+    """Full search over device keys/tags. Returns (triplets uint8 CUDA tensor of
+    TRIPLET_DTYPE records, SearchStats, DeviceSearch)."""
+    torch = nat.torch()
+    stats = SearchStats(n_fingerprints=n)
+    bounds = partition_bounds(n, cfg.partitions) if n else []
+    stats.partitions = bounds
+    ds = DeviceSearch(keys, tags, n, t, timing=timing)
+    if n == 0:
+        return torch.empty(0, dtype=torch.uint8, device="cuda"), stats, ds
+    p = len(bounds)
+    edges_h = np.array([a for a, _ in bounds] + [bounds[-1][1]], dtype=np.int64)
+    edges = torch.from_numpy(edges_h).to(keys.device)
+    stats.peak_table_entries = int(max(b - a for a, b in bounds)) * t
+    excl = int(exclusion_windows)
+    if excl < 0:
+        raise ParameterError("exclusion_windows must be >= 0")
+    ds.buckets()
+    emask = None
+    n_ex = 0
+    if cfg.occurrence_threshold is not None:
+        pk, ps, matched, _ = ds.pairs(cfg.min_matches, excl, None, edges, p)
+        emask, n_ex = ds.occurrence(pk, ps, matched, cfg.occurrence_threshold, edges, p)
+        del pk, ps
+        if n_ex == 0:
+            emask = None
+    pk, ps, matched, distinct = ds.pairs(cfg.min_matches, excl, emask, edges, p)
+    looks, pieces, mx, hist, big = ds.bucket_stats(emask, edges, p)
+    trip = ds.finalize(pk, ps, matched)
+    singles = ds.heads - ds.nb
+    stats.lookups_total = looks
+    stats.distinct_pairs = distinct
+    stats.emitted_triplets = matched
+    stats.filtered_fingerprints = n_ex
+    stats.n_queries = n - n_ex
+    stats.n_buckets = pieces + singles
+    stats.max_bucket = max(mx, 1 if singles else 0)
+    hist = hist.copy()
+    hist[1] += singles
+    stats.top_bucket_mass = _top_mass(hist, big, stats.n_buckets, n * t)
+    return trip, stats, ds
+
+
+def _empty_triplets():
+    return np.empty(0, dtype=TRIPLET_DTYPE)
+
+
+def search_signatures(sigs, cfg: SearchConfig, exclusion_windows: int = 0):
+    """Find similar pairs among an (n, t) signature matrix (lsh_search.py:222-303).
+
+    Returns (triplets, stats); triplets is a TRIPLET_DTYPE record array sorted
+    by (dt, idx1) — a host numpy array for host input, a CUDA uint8 tensor of
+    packed records for CUDA tensor input."""
+    cfg.validate()
+    torch = nat.torch()
+    on_device = nat.is_device_tensor(sigs)
+    if on_device:
+        if sigs.dim() != 2 or sigs.shape[1] != cfg.tables:
+            raise ParameterError("signature matrix does not match cfg.tables")
+        sdev = sigs.contiguous()
+        if sdev.dtype != torch.int64:
+            sdev = sdev.to(torch.int64)
+    else:
+        arr = np.ascontiguousarray(sigs, dtype=np.uint64)
+        if arr.ndim != 2 or arr.shape[1] != cfg.tables:
+            raise ParameterError("signature matrix does not match cfg.tables")
+        sdev = None
+    n = int(sdev.shape[0] if on_device else arr.shape[0])
+    if n >= 2**32:
+        raise ParameterError("more than 2**32 fingerprints are not supported")
+    t = cfg.tables
+    if n == 0:
+        stats = SearchStats(n_fingerprints=0)
+        return (_empty_triplets() if not on_device else
+                torch.empty(0, dtype=torch.uint8, device=sigs.device)), stats
+    if not on_device:
+        sdev = torch.from_numpy(arr.view(np.int64)).to("cuda")
+    W = (t + 31) // 32
+    keys = torch.empty((t, n), dtype=torch.int64, device=sdev.device)
+    tags = torch.empty((n, 16, W), dtype=torch.int32, device=sdev.device)
+    nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(tags), nat.stream())
+    trip, stats, _ = run_search(keys, tags, n, t, cfg, exclusion_windows)
+    if on_device:
+        return trip, stats
+    return trip.cpu().numpy().view(TRIPLET_DTYPE), stats
+
+
+def signatures_for_search(bits, mapping: HashMapping):
+    """Fused Min-Max kernel writing table-major keys + tags directly (no
+    row-major signature round trip). bits: CUDA int32 (n, K)."""
+    torch = nat.torch()
+    n, K = bits.shape
+    t = mapping.t
+    W = (t + 31) // 32
+    _, plan = mapping.device_plan()
+    keys = torch.empty((t, n), dtype=torch.int64, device=bits.device)
+    tags = torch.empty((n, 16, W), dtype=torch.int32, device=bits.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=bits.device)
+    nat.call("qs_minmax_signatures_search", nat.ptr(bits), n, K, nat.ptr(plan), mapping.d, t,
+             mapping.k_half, None, nat.ptr(keys), nat.ptr(tags), nat.ptr(bad), nat.stream())
+    return keys, tags, bad
+
+
+def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = None,
+                        workers: int = 1):
+    """Signature generation plus similarity search for one channel
+    (lsh_search.py:314-333). Returns (triplets, stats, mapping)."""
+    cfg.validate()
+    if mapping is None:
+        mapping = gen_hash_mapping(fps.d, cfg.tables, cfg.hash_funcs, cfg.seed)
+    if (mapping.t, mapping.k) != (cfg.tables, cfg.hash_funcs):
+        raise ConsistencyError("hash mapping does not match search config")
+    if mapping.d != fps.d:
+        raise ConsistencyError("hash mapping dimensionality does not match fingerprints")
+    torch = nat.torch()
+    bits = fps.bits
+    on_device = nat.is_device_tensor(bits)
+    if on_device:
+        bdev = bits.contiguous().to(torch.int32) if bits.dtype != torch.int32 else bits.contiguous()
+        if bdev.dim() != 2:
+            raise ParameterError("bits must be a 2-D (n, K) array")
+    else:
+        arr = np.ascontiguousarray(bits, dtype=np.uint32)
+        if arr.ndim != 2:
+            raise ParameterError("bits must be a 2-D (n, K) array")
+        if arr.shape[1] < 1:
+            raise ParameterError("fingerprints must have at least one set bit")
+        if arr.shape[0] and int(arr.max()) >= mapping.d:
+            raise ParameterError("fingerprint bit index out of range for mapping")
+        bdev = torch.from_numpy(arr.view(np.int32)).to("cuda")
+    n, K = bdev.shape
+    if K < 1:
+        raise ParameterError("fingerprints must have at least one set bit")
+    if n >= 2**32:
+        raise ParameterError("more than 2**32 fingerprints are not supported")
+    excl = exclusion_windows_for(fps, cfg)
+    if n == 0:
+        empty = _empty_triplets() if not on_device else torch.empty(0, dtype=torch.uint8, device="cuda")
+        return empty, SearchStats(n_fingerprints=0), mapping
+    keys, tags, bad = signatures_for_search(bdev, mapping)
+    if on_device and int(bad.item()):
+        raise ParameterError("fingerprint bit index out of range for mapping")
+    trip, stats, _ = run_search(keys, tags, n, cfg.tables, cfg, excl)
+    if on_device:
+        return trip, stats, mapping
+    return trip.cpu().numpy().view(TRIPLET_DTYPE), stats, mapping

@@ -1,0 +1,121 @@
+"""LSH search parity on the GPU: byte-identical triplets and identical
+SearchStats against the reference's golden runs, plus oracle comparisons on
+random and cfg1-shaped inputs (reference tests/test_lsh_search.py strategy:
+brute force, partition identity, canonical/sorted output, near-repeat
+exclusion, occurrence filter, stats fields)."""
+
+import numpy as np
+import pytest
+
+from oracle import search as osr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ls():
+    from paper_1803_09835_b200 import lsh_search
+    return lsh_search
+
+
+def _cfg(ls, c):
+    c = dict(c)
+    excl = c.pop("exclusion_windows", 0)
+    return ls.SearchConfig(**c), excl
+
+
+def _check_stats(got, want, name):
+    d = got.to_dict()
+    for k, v in want.items():
+        if isinstance(v, float):
+            assert d[k] == pytest.approx(v, rel=1e-12, abs=1e-15), (name, k, d[k], v)
+        else:
+            assert d[k] == v, (name, k, d[k], v)
+
+
+def test_golden_search_cases(ls, golden_search):
+    for name, case in golden_search.items():
+        cfg, excl = _cfg(ls, case["cfg"])
+        rec, st = ls.search_signatures(case["sigs"], cfg, exclusion_windows=excl)
+        assert rec.dtype == ls.TRIPLET_DTYPE
+        assert rec.tobytes() == case["trip"].tobytes(), name
+        _check_stats(st, case["stats"], name)
+
+
+def _oracle(sigs, cfg, excl):
+    return osr.search(sigs, tables=cfg.tables, min_matches=cfg.min_matches,
+                      partitions=cfg.partitions, occurrence_threshold=cfg.occurrence_threshold,
+                      exclusion_windows=excl)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_collide_prone_vs_oracle(ls, seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2, 400))
+    t = int(rng.choice([1, 3, 16, 32, 33, 64, 100, 128, 130]))
+    sigs = rng.integers(0, int(rng.integers(2, 30)), size=(n, t)).astype(np.uint64)
+    if rng.random() < 0.3:
+        sigs[:, :] |= np.uint64(1) << np.uint64(63)
+    m = int(rng.integers(1, t + 1))
+    p = int(rng.choice([1, 2, 3, 7]))
+    occ = [None, 0.05, 0.3, 1.0][int(rng.integers(0, 4))]
+    excl = int(rng.integers(0, 5))
+    cfg = ls.SearchConfig(tables=t, hash_funcs=2, min_matches=m, partitions=p,
+                          occurrence_threshold=occ)
+    rec, st = ls.search_signatures(sigs, cfg, exclusion_windows=excl)
+    want, wst = _oracle(sigs, cfg, excl)
+    assert rec.tobytes() == want.tobytes()
+    _check_stats(st, {k: v for k, v in wst.items() if k not in ("lookups_per_query", "selectivity")},
+                 seed)
+    if occ is None:
+        bf = osr.brute_force_triplets(sigs, m, excl)
+        assert sorted((int(a), int(b), int(c)) for a, b, c in
+                      zip(rec["dt"], rec["idx1"], rec["sim"])) == bf
+
+
+def test_partition_identity_and_device_output(ls):
+    import torch
+    rng = np.random.default_rng(6)
+    sigs = rng.integers(0, 40, size=(2000, 12)).astype(np.uint64)
+    base = None
+    for p in (1, 2, 3, 8, 64):
+        cfg = ls.SearchConfig(tables=12, hash_funcs=2, min_matches=2, partitions=p)
+        rec, st = ls.search_signatures(sigs, cfg, exclusion_windows=1)
+        if base is None:
+            base = rec.tobytes()
+            assert rec.size > 50
+        assert rec.tobytes() == base
+    dev, _ = ls.search_signatures(torch.from_numpy(sigs.view(np.int64)).cuda(),
+                                  ls.SearchConfig(tables=12, hash_funcs=2, min_matches=2),
+                                  exclusion_windows=1)
+    assert dev.is_cuda and dev.cpu().numpy().tobytes() == base
+
+
+def test_cfg1_shaped_vs_oracle(ls):
+    from oracle import minmax as omm
+    from paper_1803_09835_b200 import minmax_hash as mh
+    from paper_1803_09835_b200 import workloads
+    bits, _ = workloads.cfg1_bits(n=20000, seed=3, pair_frac=1 / 80, group_frac=1 / 1000)
+    m = mh.gen_hash_mapping(4096, 100, 4, 0)
+    sigs = mh.signatures(bits, m)
+    assert np.array_equal(sigs[:500], omm.signatures_c(bits[:500], m.values, 100, 2))
+    for occ, p, excl in [(None, 1, 0), (120 / 20000, 1, 0), (60 / 20000, 4, 3)]:
+        cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, partitions=p,
+                              occurrence_threshold=occ)
+        rec, st = ls.search_signatures(sigs, cfg, exclusion_windows=excl)
+        want, wst = _oracle(sigs, cfg, excl)
+        assert rec.tobytes() == want.tobytes(), (occ, p)
+        _check_stats(st, {k: v for k, v in wst.items()}, (occ, p))
+
+
+def test_search_config_validation(ls):
+    from paper_1803_09835_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        ls.SearchConfig(tables=0).validate()
+    with pytest.raises(ParameterError):
+        ls.SearchConfig(hash_funcs=3).validate()
+    with pytest.raises(ParameterError):
+        ls.SearchConfig(min_matches=101).validate()
+    with pytest.raises(ParameterError):
+        ls.search_signatures(np.zeros((3, 4), np.uint64), ls.SearchConfig(tables=5))
+    assert ls.PROFILES == {"baseline": (6, 5), "optimized": (8, 2)}
