@@ -63,15 +63,17 @@ int qs_minmax_signatures(const uint32_t* bits_dev, uint64_t n, uint32_t K,
                          const void* plan_dev, uint32_t d, uint32_t t, uint32_t k_half,
                          uint64_t* out_dev, uint32_t* bad_dev, void* stream);
 
-/* Same computation, table-major output for the search: keys_dev (t, n) uint64
- * holds mix64(sig) (a bijection of the signature word, so bucket equality is
- * unchanged) and tags_dev (n, 16, ceil(t/32)) uint32 the bit-sliced 16-bit
- * tags used for exact first-colliding-table dedup.  sigs_dev (n, t) may be
- * NULL when the row-major signatures are not wanted. */
+/* Same computation, search layout: keys_dev (t, n) uint64 table-major and
+ * rkeys_dev (n, t) uint64 row-major hold mix64(sig) (a bijection of the
+ * signature word, so bucket equality is unchanged) and tags_dev
+ * (n, ceil(t/32), 16) uint32 the bit-sliced 16-bit tags (plane p of word w =
+ * bit p of the tags of tables 32w..32w+31) used for exact
+ * first-colliding-table dedup.  sigs_dev (n, t) may be NULL. */
 int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K,
                                 const void* plan_dev, uint32_t d, uint32_t t,
                                 uint32_t k_half, uint64_t* sigs_dev, uint64_t* keys_dev,
-                                uint32_t* tags_dev, uint32_t* bad_dev, void* stream);
+                                uint64_t* rkeys_dev, uint32_t* tags_dev, uint32_t* bad_dev,
+                                void* stream);
 
 /* HOST-buffer drop-in for the reference's native plugin point
  * `_core.gen_signatures_range(bits, values, t, k_half, out, start, stop)`
@@ -86,60 +88,73 @@ int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
 /* ------------------------------------------------------------- LSH search
  * The search (lsh_search.search_signatures, lsh_search.py:222-303) runs as the
  * stage sequence below, orchestrated by the Python host layer which owns all
- * buffers.  Layout: keys (t, n) uint64 table-major mixed signature words;
- * tags (n, 16, W) uint32, W = ceil(t/32). */
+ * buffers.  Layouts: keys (t, n) / rkeys (n, t) uint64 mixed signature words;
+ * tags (n, W, 16) uint32, W = ceil(t/32).  A bucket list is (bstart = offset
+ * of the bucket's first member in the member-id array, bsize, btab = table). */
 
-/* Row-major signatures (n, t) -> keys (t, n) + tags.  Used when the caller
+/* Row-major signatures (n, t) -> keys + rkeys + tags.  Used when the caller
  * hands in signatures (search_signatures) rather than bits. */
-int qs_lsh_prep(const uint64_t* sigs_dev, uint64_t n, uint32_t t,
-                uint64_t* keys_dev, uint32_t* tags_dev, void* stream);
+int qs_lsh_prep(const uint64_t* sigs_dev, uint64_t n, uint32_t t, uint64_t* keys_dev,
+                uint64_t* rkeys_dev, uint32_t* tags_dev, void* stream);
 
 /* Bucket construction: per table, sort (key, id) so equal keys are contiguous
  * with ascending ids (the stable argsort of lsh_search.py:157-164).
- * ids_out_dev (t, n) uint32; keys_out_dev (t, n) uint64 sorted keys.
- * Workspace bytes from qs_lsh_bucket_ws_bytes. */
+ * ids_out_dev (t, n) uint32; keys_out_dev (t, n) uint64 sorted keys. */
 size_t qs_lsh_bucket_ws_bytes(uint64_t n, uint32_t t);
 int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t,
                          uint64_t* keys_out_dev, uint32_t* ids_out_dev,
                          void* ws_dev, size_t ws_bytes, void* stream);
 
-/* Bucket listing: non-singleton buckets (start position in the (t, n) sorted
- * arrays, size) and per-table head counts.  Two calls: first with
- * bstart_dev == NULL to count into *count_dev (uint64), then to fill. */
+/* Bucket listing (lsh_search.py:167-172 run lengths): non-singleton buckets
+ * of all tables.  Call first with bstart_dev == NULL: counts_dev[0] = number
+ * of non-singleton buckets, counts_dev[1] = number of buckets (all tables);
+ * then with arrays of that capacity to fill them. */
 size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t);
 int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t,
-                        uint64_t* bstart_dev, uint32_t* bsize_dev,
-                        uint64_t* counts_dev /* [0]=non-singleton buckets, [1]=heads */,
-                        void* ws_dev, size_t ws_bytes, void* stream);
+                        uint64_t* bstart_dev, uint32_t* bsize_dev, uint32_t* btab_dev,
+                        uint64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
-/* Search statistics from the bucket list (SearchStats, lsh_search.py:70-109):
- * lookups_total, per-partition-table bucket sizes (histogram of sizes
- * < hist_len into hist_dev uint64; larger sizes appended to big_dev with
- * count in out_dev[2]), n_buckets and max bucket.  excluded_dev (n bytes)
- * may be NULL; edges_dev holds the partition_bounds edges (p + 1 values). */
+/* SearchStats bucket fields (lsh_search.py:70-109, 295-302): lookups_total
+ * (counted before the canonical/dt/exclusion masks, :192-194), the sizes of
+ * the per-partition-table buckets (histogram of sizes < hist_len into
+ * hist_dev; larger sizes appended to big_dev), n_buckets and the max bucket.
+ * out_dev: [0] lookups, [1] partition-table buckets from non-singleton lists,
+ * [2] number of big sizes, [3] max size.  excluded_dev (n bytes) may be NULL;
+ * edges_dev holds the partition_bounds edges (p + 1 values). */
 int qs_lsh_bucket_stats(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                         const uint32_t* bsize_dev, uint64_t n_nonsingle,
                         const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p,
                         uint64_t* hist_dev, uint32_t hist_len, uint32_t* big_dev,
-                        uint64_t big_cap, uint64_t* out_dev /* [0]=lookups [1]=buckets-from-splits [2]=n_big [3]=max */,
-                        void* stream);
+                        uint64_t big_cap, uint64_t* out_dev, void* stream);
 
-/* Candidate-pair enumeration + exact collision counting + >= m threshold.
- * Every unordered pair sharing a bucket is visited in the bucket of its
- * FIRST colliding table only (exact dedup via bit-sliced tag comparison,
- * verified on the 64-bit keys), so each distinct pair is counted once with
- * sim = number of tables whose keys agree.  Applies the reference's masks
- * (canonical c < q, q - c > excl, excluded/partition rule of
- * lsh_search.py:256-287).  Emits (sortkey = (q - c) << 32 | c, sim) for
- * sim >= m into out_key/out_sim (capacity cap; the true count is always
- * written to counters_dev[1] so the caller can grow and retry);
- * counters_dev[0] += distinct pairs.  Workspace from qs_lsh_pairs_ws_bytes. */
+/* Remove excluded members from every bucket (single partition only; an
+ * excluded fingerprint can never be part of a counted pair there).  Writes
+ * the compacted member ids and bucket list (buckets keeping >= 2 members);
+ * counts_dev[0] = buckets kept, counts_dev[1] = members kept. */
+size_t qs_lsh_compact_ws_bytes(uint64_t n_nonsingle);
+int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                           const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t nb,
+                           const uint8_t* excluded_dev, uint32_t* sids2_dev,
+                           uint64_t* bstart2_dev, uint32_t* bsize2_dev, uint32_t* btab2_dev,
+                           uint64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* Candidate-pair enumeration + exact collision counting + >= m threshold
+ * (replaces _collect_pairs + the count filter, lsh_search.py:175-219, 261, 281).
+ * Every unordered pair sharing a bucket is handled only in the bucket of its
+ * FIRST colliding table (exact dedup: bit-sliced tag comparison confirmed on
+ * the 64-bit keys), so each distinct pair is seen once and sim = number of
+ * tables whose keys agree.  Masks: canonical c < q, q - c > excl, exclusion /
+ * partition rule of lsh_search.py:256-287.  mode 0: count distinct pairs and
+ * emit sim >= m; 1: emit only; 2: count only.  Emitted records are
+ * (sortkey = (q - c) << 32 | c, sim) into out_key/out_sim (capacity cap; the
+ * true count is always added to counters_dev[1] so the caller can grow and
+ * retry); counters_dev[0] += distinct pairs. */
 size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle);
 int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
-                 const uint32_t* bsize_dev, uint64_t n_nonsingle,
-                 const uint64_t* keys_dev, const uint32_t* tags_dev, uint64_t n, uint32_t t,
+                 const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t n_nonsingle,
+                 const uint64_t* rkeys_dev, const uint32_t* tags_dev, uint64_t n, uint32_t t,
                  uint32_t m, uint64_t excl, const uint8_t* excluded_dev,
-                 const uint64_t* edges_dev, uint32_t p,
+                 const uint64_t* edges_dev, uint32_t p, int mode,
                  uint64_t* out_key_dev, uint32_t* out_sim_dev, uint64_t cap,
                  unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
                  void* stream);
@@ -148,15 +163,21 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
  * filter-free enumeration: per partition, degree over within-partition
  * matched pairs, core = degree > thr * |partition|, excluded = core plus the
  * matched within-partition neighbours of core.  excluded_dev (n bytes) is
- * written; counters_dev[0] = number excluded.  Workspace: n * 4 bytes. */
+ * written; counters_dev[0] += number excluded.  Workspace: n * 4 bytes. */
 int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
                              uint64_t n_pairs, uint64_t n, double threshold,
                              const uint64_t* edges_dev, uint32_t p, uint8_t* excluded_dev,
                              unsigned long long* counters_dev, void* ws_dev, void* stream);
 
+/* Matched pairs that survive the exclusion rule (pass-2 emission of
+ * lsh_search.py:276-287), appended to out_* with *counter_dev as cursor. */
+int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
+                        uint64_t n_pairs, const uint8_t* excluded_dev,
+                        const uint64_t* edges_dev, uint32_t p, uint64_t* out_key_dev,
+                        uint32_t* out_sim_dev, unsigned long long* counter_dev, void* stream);
+
 /* Sort matched pairs by (dt, idx1) (lsh_search.py:291) and pack them into
- * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38).
- * Workspace from qs_sort_pairs_ws_bytes. */
+ * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38). */
 size_t qs_sort_pairs_ws_bytes(uint64_t n);
 int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_pairs,
                     uint32_t key_bits, uint8_t* triplets_dev, void* ws_dev, size_t ws_bytes,

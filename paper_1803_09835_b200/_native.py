@@ -34,19 +34,22 @@ SIGNATURES = {
     "qs_minmax_plan": (_int, [_p, _u32, _u32, _p, _p]),
     "qs_minmax_signatures": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p]),
     "qs_minmax_signatures_search": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p,
-                                           _p, _p]),
+                                           _p, _p, _p]),
     "qs_gen_signatures_range": (_int, [_p, _u64, _u32, _p, _u32, _u32, _i32, _i32, _p, _u64,
                                        _u64]),
-    "qs_lsh_prep": (_int, [_p, _u64, _u32, _p, _p, _p]),
+    "qs_lsh_prep": (_int, [_p, _u64, _u32, _p, _p, _p, _p]),
     "qs_lsh_bucket_ws_bytes": (_sz, [_u64, _u32]),
     "qs_lsh_build_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _sz, _p]),
     "qs_lsh_list_ws_bytes": (_sz, [_u64, _u32]),
-    "qs_lsh_list_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _sz, _p]),
+    "qs_lsh_list_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _p, _sz, _p]),
     "qs_lsh_bucket_stats": (_int, [_p, _p, _p, _u64, _p, _p, _u32, _p, _u32, _p, _u64, _p, _p]),
+    "qs_lsh_compact_ws_bytes": (_sz, [_u64]),
+    "qs_lsh_compact_buckets": (_int, [_p, _p, _p, _p, _u64, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "qs_lsh_pairs_ws_bytes": (_sz, [_u64]),
-    "qs_lsh_pairs": (_int, [_p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
-                            _p, _p, _u64, _p, _p, _sz, _p]),
+    "qs_lsh_pairs": (_int, [_p, _p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
+                            _int, _p, _p, _u64, _p, _p, _sz, _p]),
     "qs_lsh_occurrence_filter": (_int, [_p, _p, _u64, _u64, _dbl, _p, _u32, _p, _p, _p, _p]),
+    "qs_lsh_filter_pairs": (_int, [_p, _p, _u64, _p, _p, _u32, _p, _p, _p, _p]),
     "qs_sort_pairs_ws_bytes": (_sz, [_u64]),
     "qs_lsh_finalize": (_int, [_p, _p, _u64, _u32, _p, _p, _sz, _p]),
     "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),

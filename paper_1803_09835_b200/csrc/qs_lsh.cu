@@ -7,42 +7,139 @@
 //
 // B200 design:
 //   * keys (t, n) = mix64(signature word) (a bijection, so bucket equality is
-//     exactly the reference's) + bit-sliced 16-bit tags (n, 16, W) per row;
+//     exactly the reference's), the same keys row-major (n, t) for exact
+//     verification, and bit-sliced 16-bit tags (n, W, 16) per row
+//     (W = ceil(t/32): plane p of word w holds bit p of the tags of tables
+//     32w..32w+31);
 //   * buckets = per-table stable (key, id) sort, ids ascending in a bucket;
 //   * pair enumeration inside buckets, each unordered pair handled ONLY in
-//     the bucket of its first colliding table: earlier tables are screened by
-//     64 LOP3s on the tag planes and confirmed on the 64-bit keys, the total
-//     collision count is the popcount of the tag-match mask (confirmed on the
-//     keys only when it could reach m).  No (pair, table) key is ever
-//     materialised and no global hash table is needed: HBM traffic is O(n*t)
-//     while the per-hit work is register/shared-memory ALU work.
-#include "qs_common.cuh"
+//     the bucket of its first colliding table: earlier tables are screened
+//     with 16 LOP3s per 32-table word on the tag planes (only the words up to
+//     the bucket's table: warp-uniform) and confirmed on the 64-bit keys; the
+//     collision count is screened on 8 planes and made exact (16 planes + key
+//     confirmation) only when it could reach m.  No (pair, table) key is ever
+//     materialised and no global hash table is needed.
+//   * occurrence filter: pass 1 ("matched" mode) collects pairs with >= m
+//     collisions, the filter marks excluded fingerprints, pass 2 ("distinct"
+//     mode) counts distinct pairs over buckets with the excluded members
+//     removed (partitions == 1) or masked (partitions > 1).
+#include "qs_lsh.cuh"
 
 namespace qs {
 
-int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
-                     uint32_t key_bits, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
-                     size_t ws_bytes, int* in_alt, cudaStream_t st);
-size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments);
+// ------------------------------------------------------------------ scan
+// Multi-block exclusive scan of uint64 (in place allowed).
+constexpr int SCAN_T = 512;
+constexpr int SCAN_I = 8;
+constexpr uint64_t SCAN_TILE = SCAN_T * SCAN_I;
 
-__device__ __forceinline__ uint64_t mix_key(uint64_t s) { return fmix64(s ^ GOLDEN64); }
-
-// partition index of fingerprint i: edges[k] <= i < edges[k+1]
-__device__ __forceinline__ uint32_t part_of(const uint64_t* __restrict__ edges, uint32_t p,
-                                            uint64_t i) {
-    uint32_t lo = 0, hi = p;  // invariant edges[lo] <= i < edges[hi]
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(edges + mid) <= i) lo = mid;
-        else hi = mid;
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* wsum, uint64_t* total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
     }
-    return lo;
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (uint32_t)o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t r = (warp ? wsum[warp - 1] : 0) + x - v;
+    if (total) *total = wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(const uint64_t* __restrict__ in, uint64_t len,
+                                                        uint64_t* __restrict__ part) {
+    __shared__ uint64_t red[SCAN_T / 32];
+    const uint64_t base = blockIdx.x * SCAN_TILE;
+    uint64_t s = 0;
+    for (int e = 0; e < SCAN_I; ++e) {
+        uint64_t i = base + (uint64_t)e * SCAN_T + threadIdx.x;
+        if (i < len) s += in[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < SCAN_T / 32; ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(uint64_t* __restrict__ a, uint64_t len,
+                                                   uint64_t* __restrict__ total) {
+    __shared__ uint64_t ws[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < len; b0 += 1024) {
+        const uint64_t i = b0 + threadIdx.x;
+        const uint64_t v = i < len ? a[i] : 0;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan(v, ws, &tot);
+        if (i < len) a[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_down(const uint64_t* __restrict__ in, uint64_t len,
+                                                      const uint64_t* __restrict__ part,
+                                                      uint64_t* __restrict__ out) {
+    __shared__ uint64_t ws[32];
+    const uint64_t base = blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_I;
+    uint64_t v[SCAN_I], s = 0;
+#pragma unroll
+    for (int e = 0; e < SCAN_I; ++e) {
+        v[e] = (base + e < len) ? in[base + e] : 0;
+        s += v[e];
+    }
+    uint64_t ex = block_excl_scan(s, ws, nullptr) + part[blockIdx.x];
+#pragma unroll
+    for (int e = 0; e < SCAN_I; ++e) {
+        if (base + e < len) out[base + e] = ex;
+        ex += v[e];
+    }
+}
+
+size_t scan_ws_bytes(uint64_t len) { return ((len + SCAN_TILE - 1) / SCAN_TILE + 1) * 8 + 64; }
+
+// out[i] = sum(in[0..i)); *total (device) = sum(in) if total != nullptr.
+int scan_u64(const uint64_t* in, uint64_t* out, uint64_t len, uint64_t* total, void* ws,
+             cudaStream_t st) {
+    if (len == 0) {
+        if (total) QS_CUDA(cudaMemsetAsync(total, 0, 8, st), "memset");
+        return QS_OK;
+    }
+    const uint64_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
+    uint64_t* part = (uint64_t*)ws;
+    k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, st>>>(in, len, part);
+    k_scan_top<<<1, 1024, 0, st>>>(part, nb, total);
+    k_scan_down<<<(unsigned)nb, SCAN_T, 0, st>>>(in, len, part, out);
+    QS_CHECK_LAUNCH("scan");
+    return QS_OK;
 }
 
 // ------------------------------------------------------------------- prep
-// Row-major signatures -> table-major keys + bit-sliced tags (one warp per row).
+// Row-major signatures -> table-major keys, row-major keys, bit-sliced tags.
 __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs, uint64_t n,
                                               uint32_t t, uint64_t* __restrict__ keys,
+                                              uint64_t* __restrict__ rkeys,
                                               uint32_t* __restrict__ tags) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -55,6 +152,7 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
             if (i < t) {
                 key = mix_key(sigs[row * t + i]);
                 keys[(uint64_t)i * n + row] = key;
+                rkeys[row * t + i] = key;
             }
             const uint32_t tag = (uint32_t)key & 0xFFFFu;
             uint32_t plane = 0;
@@ -63,7 +161,7 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
                 uint32_t word = __ballot_sync(0xffffffffu, (i < t) && ((tag >> b) & 1u));
                 if (lane == (uint32_t)b) plane = word;
             }
-            if (lane < 16) tags[(row * 16 + lane) * W + wr] = plane;
+            if (lane < 16) tags[(row * W + wr) * 16 + lane] = plane;
         }
     }
 }
@@ -77,8 +175,8 @@ __global__ void k_iota_segments(uint32_t* __restrict__ ids, uint64_t n, uint32_t
 
 // --------------------------------------------------------------- listing
 // Ordered compaction of bucket heads/tails over the sorted (t, n) key array.
-// kind 0: heads of non-singleton buckets, kind 1: tails of non-singleton
-// buckets, kind 2: all heads (count only).
+// kind 0: heads of non-singleton buckets, 1: tails of non-singleton buckets,
+// 2: all heads (count only).
 __device__ __forceinline__ bool list_flag(const uint64_t* __restrict__ k, uint64_t n,
                                           uint64_t g, int kind) {
     const uint64_t pos = g % n;
@@ -109,44 +207,6 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_count(const uint64_t* __r
         for (int w = 0; w < LIST_THREADS / 32; ++w) s += red[w];
         counts[blockIdx.x] = s;
     }
-}
-
-// single-CTA exclusive scan of `len` uint64 values in place; total to *total
-__global__ void __launch_bounds__(1024) k_scan_u64(uint64_t* __restrict__ a, uint64_t len,
-                                                   uint64_t* __restrict__ total) {
-    __shared__ uint64_t ws[32];
-    __shared__ uint64_t carry;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (uint64_t b0 = 0; b0 < len; b0 += 1024) {
-        const uint64_t i = b0 + threadIdx.x;
-        const uint64_t v = i < len ? a[i] : 0;
-        uint64_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (uint32_t)o) x += y;
-        }
-        if (lane == 31) ws[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint64_t w = ws[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= (uint32_t)o) w += y;
-            }
-            ws[lane] = w;
-        }
-        __syncthreads();
-        const uint64_t incl = carry + (warp ? ws[warp - 1] : 0) + x;
-        if (i < len) a[i] = incl - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = incl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0 && total) *total = carry;
 }
 
 // kind 0 writes global positions (uint64) of non-singleton heads; kind 1
@@ -188,29 +248,56 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
 
 // bsize holds in-table tail positions on entry, bucket sizes on exit
 __global__ void k_make_sizes(const uint64_t* __restrict__ heads, const uint64_t* __restrict__ nbp,
-                             uint64_t n, uint32_t* __restrict__ bsize) {
+                             uint64_t n, uint32_t* __restrict__ bsize, uint32_t* __restrict__ btab) {
     const uint64_t nb = *nbp;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
-         i += (uint64_t)gridDim.x * blockDim.x)
+         i += (uint64_t)gridDim.x * blockDim.x) {
         bsize[i] = (uint32_t)(bsize[i] - heads[i] % n + 1);
+        btab[i] = (uint32_t)(heads[i] / n);
+    }
 }
 
 // ----------------------------------------------------------------- stats
+constexpr int ST_HIST = 256;
+
+__device__ __forceinline__ void stats_piece(uint64_t nP, unsigned long long* sh,
+                                            unsigned long long* __restrict__ hist,
+                                            uint32_t hist_len, uint32_t* __restrict__ big,
+                                            uint64_t big_cap, unsigned long long* __restrict__ out,
+                                            unsigned long long& mx) {
+    if (nP > mx) mx = nP;
+    if (nP < ST_HIST) atomicAdd(sh + nP, 1ULL);
+    else if (nP < hist_len) atomicAdd(hist + nP, 1ULL);
+    else {
+        unsigned long long k = atomicAdd(out + 2, 1ULL);
+        if (k < big_cap) big[k] = (uint32_t)nP;
+    }
+}
+
 // One thread per non-singleton bucket: partition split, lookups, size histogram.
-__global__ void k_bucket_stats(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
-                               const uint32_t* __restrict__ bsize, uint64_t nb,
-                               const uint8_t* __restrict__ excl_mask,
-                               const uint64_t* __restrict__ edges, uint32_t p,
-                               unsigned long long* __restrict__ hist, uint32_t hist_len,
-                               uint32_t* __restrict__ big, uint64_t big_cap,
-                               unsigned long long* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_bucket_stats(
+    const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
+    const uint32_t* __restrict__ bsize, uint64_t nb, const uint8_t* __restrict__ excl_mask,
+    const uint64_t* __restrict__ edges, uint32_t p, unsigned long long* __restrict__ hist,
+    uint32_t hist_len, uint32_t* __restrict__ big, uint64_t big_cap,
+    unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long sh[ST_HIST];
+    for (int i = threadIdx.x; i < ST_HIST; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    unsigned long long looks = 0, pieces = 0, mx = 0;
+    const bool simple = (p <= 1) && (excl_mask == nullptr);
     for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
          b += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t st = bstart[b];
         const uint64_t s = bsize[b];
-        unsigned long long looks = 0, pieces = 0, mx = 0;
-        uint64_t cum_e = 0, e_tot = 0;
-        uint64_t j = 0;
+        if (simple) {
+            looks += s * (s - 1);
+            ++pieces;
+            stats_piece(s, sh, hist, hist_len, big, big_cap, out, mx);
+            continue;
+        }
+        const uint64_t st = bstart[b];
+        uint64_t cum_e = 0, e_tot = 0, j = 0;
+        unsigned long long lb = 0;
         while (j < s) {
             const uint64_t id = sids[st + j];
             const uint32_t P = p > 1 ? part_of(edges, p, id) : 0;
@@ -225,255 +312,69 @@ __global__ void k_bucket_stats(const uint32_t* __restrict__ sids, const uint64_t
             }
             cum_e += eP;
             e_tot += eP;
-            looks += nP * (s - cum_e);
+            lb += nP * (s - cum_e);
             ++pieces;
-            if (nP > mx) mx = nP;
-            if (nP < hist_len) atomicAdd(hist + nP, 1ULL);
-            else {
-                unsigned long long k = atomicAdd(out + 2, 1ULL);
-                if (k < big_cap) big[k] = (uint32_t)nP;
-            }
+            stats_piece(nP, sh, hist, hist_len, big, big_cap, out, mx);
         }
-        looks -= (s - e_tot);
-        atomicAdd(out + 0, looks);
-        atomicAdd(out + 1, pieces);
-        atomicMax(out + 3, mx);
+        looks += lb - (s - e_tot);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        looks += __shfl_down_sync(0xffffffffu, looks, o);
+        pieces += __shfl_down_sync(0xffffffffu, pieces, o);
+        unsigned long long y = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (looks) atomicAdd(out + 0, looks);
+        if (pieces) atomicAdd(out + 1, pieces);
+        if (mx) atomicMax(out + 3, mx);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ST_HIST; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, sh[i]);
+}
+
+// -------------------------------------------------- exclusion compaction
+// partitions == 1 only: an excluded member can never be part of a counted
+// pair, so it is removed from the bucket before enumeration.
+__global__ void k_keep_count(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
+                             const uint32_t* __restrict__ bsize, uint64_t nb,
+                             const uint8_t* __restrict__ ex, uint64_t* __restrict__ cnt,
+                             uint64_t* __restrict__ flag) {
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t st = bstart[b];
+        const uint32_t s = bsize[b];
+        uint32_t k = 0;
+        for (uint32_t j = 0; j < s; ++j) k += ex[sids[st + j]] == 0;
+        cnt[b] = k >= 2 ? k : 0;
+        flag[b] = k >= 2 ? 1 : 0;
     }
 }
 
-// ----------------------------------------------------------------- pairs
-constexpr int PAIR_WARPS = 4;
-constexpr uint32_t GRAB = 16;
-
-__device__ __forceinline__ bool keys_equal(const uint64_t* __restrict__ keys, uint64_t n,
-                                           uint32_t tt, uint64_t a, uint64_t b) {
-    return __ldg(keys + (uint64_t)tt * n + a) == __ldg(keys + (uint64_t)tt * n + b);
-}
-
-// W = 32-table words per tag plane (compile-time, 1..4).
-template <int W>
-__global__ void __launch_bounds__(PAIR_WARPS * 32) k_pairs(
-    const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
-    const uint32_t* __restrict__ bsize, const uint64_t* __restrict__ chunk_off, uint64_t nb,
-    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
-    uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask,
-    const uint64_t* __restrict__ edges, uint32_t p, uint64_t* __restrict__ out_key,
-    uint32_t* __restrict__ out_sim, uint64_t cap, unsigned long long* __restrict__ counters,
-    unsigned long long* __restrict__ work) {
-    __shared__ __align__(16) uint32_t rows[PAIR_WARPS][32][16 * W];
-    __shared__ uint32_t rid[PAIR_WARPS][32];
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t total_chunks = chunk_off[nb];
-    const uint32_t last_mask = (t & 31) ? ((1u << (t & 31)) - 1u) : 0xFFFFFFFFu;
-    unsigned long long distinct = 0;
-
-    while (true) {
-        unsigned long long g0 = 0;
-        if (lane == 0) g0 = atomicAdd(work, (unsigned long long)GRAB);
-        g0 = __shfl_sync(0xffffffffu, g0, 0);
-        if (g0 >= total_chunks) break;
-        const uint64_t g1 = min((uint64_t)g0 + GRAB, total_chunks);
-        // bucket of chunk g0: largest b with chunk_off[b] <= g0
-        uint64_t lo = 0, hi = nb;
-        while (hi - lo > 1) {
-            uint64_t mid = (lo + hi) >> 1;
-            if (chunk_off[mid] <= g0) lo = mid;
-            else hi = mid;
+__global__ void k_keep_write(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
+                             const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                             uint64_t nb, const uint8_t* __restrict__ ex,
+                             const uint64_t* __restrict__ cnt_raw, const uint64_t* __restrict__ mem_off,
+                             const uint64_t* __restrict__ slot, uint32_t* __restrict__ sids2,
+                             uint64_t* __restrict__ bstart2, uint32_t* __restrict__ bsize2,
+                             uint32_t* __restrict__ btab2) {
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = cnt_raw[b];
+        if (!k) continue;
+        const uint64_t st = bstart[b], o = mem_off[b], sl = slot[b];
+        const uint32_t s = bsize[b];
+        uint64_t w = o;
+        for (uint32_t j = 0; j < s; ++j) {
+            const uint32_t x = sids[st + j];
+            if (!ex[x]) sids2[w++] = x;
         }
-        uint64_t b = lo;
-        for (uint64_t g = g0; g < g1; ++g) {
-            while (chunk_off[b + 1] <= g) ++b;
-            const uint64_t c = g - chunk_off[b];
-            const uint64_t st = bstart[b];
-            const uint32_t s = bsize[b];
-            const uint32_t table = (uint32_t)(st / n);
-            const uint32_t wt = table >> 5, bt = table & 31;
-            const uint32_t i = (uint32_t)c * 32 + lane;
-            const bool active = i < s;
-            const uint32_t a = active ? sids[st + i] : 0;
-            uint32_t A[16][W];
-            if (active) {
-                const uint4* src = (const uint4*)(tags + (uint64_t)a * 16 * W);
-                if (W == 4) {
-#pragma unroll
-                    for (int pl = 0; pl < 16; ++pl) {
-                        uint4 v = __ldg(src + pl);
-                        A[pl][0] = v.x; A[pl][1 % W] = v.y; A[pl][2 % W] = v.z; A[pl][3 % W] = v.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int pl = 0; pl < 16; ++pl)
-#pragma unroll
-                        for (int w = 0; w < W; ++w) A[pl][w] = __ldg(tags + ((uint64_t)a * 16 + pl) * W + w);
-                }
-            } else {
-#pragma unroll
-                for (int pl = 0; pl < 16; ++pl)
-#pragma unroll
-                    for (int w = 0; w < W; ++w) A[pl][w] = 0;
-            }
-            const bool a_ex = emask && active && emask[a];
-            const uint32_t a_part = (emask && p > 1 && active) ? part_of(edges, p, a) : 0;
-            for (uint32_t jb = (uint32_t)c * 32; jb < s; jb += 32) {
-                const uint32_t jj = jb + lane;
-                __syncwarp();
-                if (jj < s) {
-                    const uint32_t bid = sids[st + jj];
-                    rid[warp][lane] = bid;
-                    const uint4* src = (const uint4*)(tags + (uint64_t)bid * 16 * W);
-                    uint4* dst = (uint4*)&rows[warp][lane][0];
-#pragma unroll
-                    for (int q = 0; q < 4 * W; ++q) dst[q] = __ldg(src + q);
-                }
-                __syncwarp();
-                const uint32_t un = min(32u, s - jb);
-                for (uint32_t u = 0; u < un; ++u) {
-                    const uint32_t j = jb + u;
-                    if (!(active && j > i)) continue;
-                    const uint32_t bid = rid[warp][u];
-                    const uint64_t dt = (uint64_t)bid - a;  // ids ascend within a bucket
-                    if (dt <= excl) continue;
-                    if (emask) {
-                        if (a_ex) continue;
-                        if (emask[bid] && (p <= 1 || part_of(edges, p, bid) == a_part)) continue;
-                    }
-                    uint32_t M[W];
-#pragma unroll
-                    for (int w = 0; w < W; ++w) M[w] = 0xFFFFFFFFu;
-                    const uint4* rb = (const uint4*)&rows[warp][u][0];
-                    if (W == 4) {
-#pragma unroll
-                        for (int pl = 0; pl < 16; ++pl) {
-                            const uint4 v = rb[pl];
-                            M[0] &= ~(A[pl][0] ^ v.x);
-                            M[1 % W] &= ~(A[pl][1 % W] ^ v.y);
-                            M[2 % W] &= ~(A[pl][2 % W] ^ v.z);
-                            M[3 % W] &= ~(A[pl][3 % W] ^ v.w);
-                        }
-                    } else {
-                        const uint32_t* rw = &rows[warp][u][0];
-#pragma unroll
-                        for (int pl = 0; pl < 16; ++pl)
-#pragma unroll
-                            for (int w = 0; w < W; ++w) M[w] &= ~(A[pl][w] ^ rw[pl * W + w]);
-                    }
-                    M[W - 1] &= last_mask;
-                    // earlier tables (first-colliding-table rule)
-                    bool first = true;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        if ((uint32_t)w > wt) break;
-                        uint32_t e = (uint32_t)w < wt ? M[w] : (M[w] & ((1u << bt) - 1u));
-                        while (e && first) {
-                            const uint32_t tt = w * 32 + __ffs(e) - 1;
-                            e &= e - 1;
-                            if (keys_equal(keys, n, tt, a, bid)) first = false;
-                        }
-                    }
-                    if (!first) continue;
-                    ++distinct;
-                    uint32_t tot = 0;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) tot += __popc(M[w]);
-                    if (tot < m) continue;
-                    uint32_t exact = 1;
-#pragma unroll
-                    for (int w = 0; w < W; ++w) {
-                        uint32_t e = M[w];
-                        if ((uint32_t)w == wt) e &= ~(1u << bt);
-                        while (e) {
-                            const uint32_t tt = w * 32 + __ffs(e) - 1;
-                            e &= e - 1;
-                            exact += keys_equal(keys, n, tt, a, bid);
-                        }
-                    }
-                    if (exact >= m) {
-                        const unsigned long long pos = atomicAdd(counters + 1, 1ULL);
-                        if (pos < cap) {
-                            out_key[pos] = (dt << 32) | a;
-                            out_sim[pos] = exact;
-                        }
-                    }
-                }
-            }
-        }
+        bstart2[sl] = o;
+        bsize2[sl] = (uint32_t)k;
+        btab2[sl] = btab[b];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
-    if (lane == 0 && distinct) atomicAdd(counters + 0, distinct);
-}
-
-// Generic path for t > 128: tag words read from global memory per pair.
-__global__ void __launch_bounds__(256) k_pairs_generic(
-    const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
-    const uint32_t* __restrict__ bsize, const uint64_t* __restrict__ chunk_off, uint64_t nb,
-    const uint64_t* __restrict__ keys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
-    uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask,
-    const uint64_t* __restrict__ edges, uint32_t p, uint64_t* __restrict__ out_key,
-    uint32_t* __restrict__ out_sim, uint64_t cap, unsigned long long* __restrict__ counters) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t W = (t + 31) >> 5;
-    const uint64_t total_chunks = chunk_off[nb];
-    unsigned long long distinct = 0;
-    for (uint64_t g = gwarp; g < total_chunks; g += nwarps) {
-        uint64_t lo = 0, hi = nb;
-        while (hi - lo > 1) {
-            uint64_t mid = (lo + hi) >> 1;
-            if (chunk_off[mid] <= g) lo = mid;
-            else hi = mid;
-        }
-        const uint64_t b = lo, c = g - chunk_off[b], st = bstart[b];
-        const uint32_t s = bsize[b], table = (uint32_t)(st / n);
-        const uint32_t i = (uint32_t)c * 32 + lane;
-        if (i >= s) continue;
-        const uint32_t a = sids[st + i];
-        const bool a_ex = emask && emask[a];
-        const uint32_t a_part = (emask && p > 1) ? part_of(edges, p, a) : 0;
-        for (uint32_t j = i + 1; j < s; ++j) {
-            const uint32_t bid = sids[st + j];
-            const uint64_t dt = (uint64_t)bid - a;
-            if (dt <= excl) continue;
-            if (emask && (a_ex || (emask[bid] && (p <= 1 || part_of(edges, p, bid) == a_part)))) continue;
-            bool first = true;
-            uint32_t tot = 0, exact = 0;
-            for (uint32_t w = 0; w < W; ++w) {
-                uint32_t M = 0xFFFFFFFFu;
-                for (int pl = 0; pl < 16; ++pl)
-                    M &= ~(tags[((uint64_t)a * 16 + pl) * W + w] ^ tags[((uint64_t)bid * 16 + pl) * W + w]);
-                if (w == W - 1 && (t & 31)) M &= (1u << (t & 31)) - 1u;
-                uint32_t e = M;
-                while (e) {
-                    const uint32_t tt = w * 32 + __ffs(e) - 1;
-                    e &= e - 1;
-                    if (keys_equal(keys, n, tt, a, bid)) {
-                        if (tt < table) first = false;
-                        ++exact;
-                    }
-                }
-                tot += __popc(M);
-            }
-            (void)tot;
-            if (!first) continue;
-            ++distinct;
-            if (exact >= m) {
-                const unsigned long long pos = atomicAdd(counters + 1, 1ULL);
-                if (pos < cap) {
-                    out_key[pos] = (dt << 32) | a;
-                    out_sim[pos] = exact;
-                }
-            }
-        }
-    }
-    atomicAdd(counters + 0, distinct);
-}
-
-__global__ void k_chunk_counts(const uint32_t* __restrict__ bsize, uint64_t nb,
-                               uint64_t* __restrict__ off) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        off[i] = (bsize[i] + 31) / 32;
 }
 
 // ------------------------------------------------------------ occurrence
@@ -528,6 +429,24 @@ __global__ void k_occ_finish(uint8_t* __restrict__ ex, uint64_t n,
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// matched pairs of the filter-free pass that survive the exclusion rule
+__global__ void k_filter_pairs(const uint64_t* __restrict__ pk, const uint32_t* __restrict__ ps,
+                               uint64_t np, const uint8_t* __restrict__ ex,
+                               const uint64_t* __restrict__ edges, uint32_t p,
+                               uint64_t* __restrict__ opk, uint32_t* __restrict__ ops,
+                               unsigned long long* __restrict__ counter) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = pk[i];
+        const uint64_t c = k & 0xFFFFFFFFull, q = c + (k >> 32);
+        if (ex[c]) continue;
+        if (ex[q] && (p <= 1 || part_of(edges, p, c) == part_of(edges, p, q))) continue;
+        const unsigned long long o = atomicAdd(counter, 1ULL);
+        opk[o] = k;
+        ops[o] = ps[i];
+    }
+}
+
 // -------------------------------------------------------------- finalize
 __global__ void k_pack_triplets(const uint64_t* __restrict__ key, const uint32_t* __restrict__ sim,
                                 uint64_t np, uint32_t* __restrict__ out) {
@@ -544,6 +463,13 @@ __global__ void k_pack_triplets(const uint64_t* __restrict__ key, const uint32_t
     }
 }
 
+int num_sms() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
 }  // namespace qs
 
 using namespace qs;
@@ -551,10 +477,11 @@ using namespace qs;
 extern "C" {
 
 int qs_lsh_prep(const uint64_t* sigs_dev, uint64_t n, uint32_t t, uint64_t* keys_dev,
-                uint32_t* tags_dev, void* stream) {
+                uint64_t* rkeys_dev, uint32_t* tags_dev, void* stream) {
     QS_ARG(t >= 1, "tables must be >= 1");
     if (n == 0) return QS_OK;
-    k_prep<<<qs_blocks(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(sigs_dev, n, t, keys_dev, tags_dev);
+    k_prep<<<qs_blocks(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(sigs_dev, n, t, keys_dev,
+                                                                      rkeys_dev, tags_dev);
     QS_CHECK_LAUNCH("k_prep");
     return QS_OK;
 }
@@ -598,12 +525,12 @@ static uint64_t list_blocks(uint64_t total) {
 
 size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t) {
     uint64_t b = list_blocks(n * t);
-    return (size_t)(b + 1) * 8 * 3 + 256;
+    return (size_t)(b + 1) * 8 + scan_ws_bytes(b) + 256;
 }
 
 int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint64_t* bstart_dev,
-                        uint32_t* bsize_dev, uint64_t* counts_dev, void* ws_dev, size_t ws_bytes,
-                        void* stream) {
+                        uint32_t* bsize_dev, uint32_t* btab_dev, uint64_t* counts_dev,
+                        void* ws_dev, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     QS_ARG(ws_bytes >= qs_lsh_list_ws_bytes(n, t), "list workspace too small");
     const uint64_t total = n * t;
@@ -614,21 +541,25 @@ int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint6
     const uint64_t B = list_blocks(total);
     const uint64_t chunk = (total + B - 1) / B;
     uint64_t* cnt = (uint64_t*)ws_dev;
+    void* sws = (void*)(((uintptr_t)(cnt + B + 1) + 63) & ~(uintptr_t)63);
     if (bstart_dev == nullptr) {
         k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, 0, cnt);
-        k_scan_u64<<<1, 1024, 0, st>>>(cnt, B, counts_dev + 0);
+        int rc = scan_u64(cnt, cnt, B, counts_dev + 0, sws, st);
+        if (rc) return rc;
         k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, 2, cnt);
-        k_scan_u64<<<1, 1024, 0, st>>>(cnt, B, counts_dev + 1);
+        rc = scan_u64(cnt, cnt, B, counts_dev + 1, sws, st);
+        if (rc) return rc;
         QS_CHECK_LAUNCH("list count");
         return QS_OK;
     }
     for (int kind = 0; kind < 2; ++kind) {
         k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, kind, cnt);
-        k_scan_u64<<<1, 1024, 0, st>>>(cnt, B, kind == 0 ? counts_dev : nullptr);
+        int rc = scan_u64(cnt, cnt, B, kind == 0 ? counts_dev : nullptr, sws, st);
+        if (rc) return rc;
         k_list_write<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, kind, cnt, bstart_dev,
                                                  bsize_dev);
     }
-    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev);
+    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev, btab_dev);
     QS_CHECK_LAUNCH("list buckets");
     return QS_OK;
 }
@@ -639,54 +570,42 @@ int qs_lsh_bucket_stats(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                         uint64_t* hist_dev, uint32_t hist_len, uint32_t* big_dev, uint64_t big_cap,
                         uint64_t* out_dev, void* stream) {
     if (n_nonsingle == 0) return QS_OK;
-    k_bucket_stats<<<qs_blocks(n_nonsingle, 128), 128, 0, (cudaStream_t)stream>>>(
+    QS_ARG(hist_len >= ST_HIST, "hist_len must be >= %d", ST_HIST);
+    k_bucket_stats<<<qs_blocks(n_nonsingle, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
         sids_dev, bstart_dev, bsize_dev, n_nonsingle, excluded_dev, edges_dev, p,
         (unsigned long long*)hist_dev, hist_len, big_dev, big_cap, (unsigned long long*)out_dev);
     QS_CHECK_LAUNCH("k_bucket_stats");
     return QS_OK;
 }
 
-size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle) {
-    return (size_t)(n_nonsingle + 1) * 8 + (qs_lsh_list_ws_bytes(n_nonsingle, 1)) + 512;
+size_t qs_lsh_compact_ws_bytes(uint64_t n_nonsingle) {
+    return (size_t)(n_nonsingle + 1) * 8 * 3 + scan_ws_bytes(n_nonsingle + 1) + 512;
 }
 
-int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
-                 uint64_t n_nonsingle, const uint64_t* keys_dev, const uint32_t* tags_dev,
-                 uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* excluded_dev,
-                 const uint64_t* edges_dev, uint32_t p, uint64_t* out_key_dev,
-                 uint32_t* out_sim_dev, uint64_t cap, unsigned long long* counters_dev,
-                 void* ws_dev, size_t ws_bytes, void* stream) {
+int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                           const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t nb,
+                           const uint8_t* excluded_dev, uint32_t* sids2_dev, uint64_t* bstart2_dev,
+                           uint32_t* bsize2_dev, uint32_t* btab2_dev, uint64_t* counts_dev,
+                           void* ws_dev, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    QS_ARG(ws_bytes >= qs_lsh_pairs_ws_bytes(n_nonsingle), "pairs workspace too small");
-    QS_ARG(m >= 1 && m <= t, "min_matches must be in [1, tables]");
-    if (n_nonsingle == 0) return QS_OK;
-    uint64_t* off = (uint64_t*)ws_dev;
-    unsigned long long* work = (unsigned long long*)(off + n_nonsingle + 1);
-    k_chunk_counts<<<qs_blocks(n_nonsingle, 256), 256, 0, st>>>(bsize_dev, n_nonsingle, off);
-    k_scan_u64<<<1, 1024, 0, st>>>(off, n_nonsingle + 1, nullptr);
-    QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint32_t W = (t + 31) >> 5;
-#define QS_PAIRS(WW)                                                                              \
-    k_pairs<WW><<<sms * 8, PAIR_WARPS * 32, 0, st>>>(sids_dev, bstart_dev, bsize_dev, off,        \
-                                                    n_nonsingle, keys_dev, tags_dev, n, t, m, excl, \
-                                                    excluded_dev, edges_dev, p, out_key_dev,     \
-                                                    out_sim_dev, cap, counters_dev, work)
-    switch (W) {
-        case 1: QS_PAIRS(1); break;
-        case 2: QS_PAIRS(2); break;
-        case 3: QS_PAIRS(3); break;
-        case 4: QS_PAIRS(4); break;
-        default:
-            k_pairs_generic<<<sms * 8, 256, 0, st>>>(sids_dev, bstart_dev, bsize_dev, off, n_nonsingle,
-                                                   keys_dev, tags_dev, n, t, m, excl, excluded_dev,
-                                                   edges_dev, p, out_key_dev, out_sim_dev, cap,
-                                                   counters_dev);
+    QS_ARG(ws_bytes >= qs_lsh_compact_ws_bytes(nb), "compact workspace too small");
+    if (nb == 0) {
+        QS_CUDA(cudaMemsetAsync(counts_dev, 0, 16, st), "memset");
+        return QS_OK;
     }
-#undef QS_PAIRS
-    QS_CHECK_LAUNCH("k_pairs");
+    uint64_t* cnt = (uint64_t*)ws_dev;
+    uint64_t* off = cnt + (nb + 1);
+    uint64_t* slot = off + (nb + 1);
+    void* sws = (void*)(((uintptr_t)(slot + nb + 1) + 63) & ~(uintptr_t)63);
+    const unsigned g = qs_blocks(nb, 256);
+    k_keep_count<<<g, 256, 0, st>>>(sids_dev, bstart_dev, bsize_dev, nb, excluded_dev, cnt, slot);
+    int rc = scan_u64(cnt, off, nb, counts_dev + 1, sws, st);
+    if (rc) return rc;
+    rc = scan_u64(slot, slot, nb, counts_dev + 0, sws, st);
+    if (rc) return rc;
+    k_keep_write<<<g, 256, 0, st>>>(sids_dev, bstart_dev, bsize_dev, btab_dev, nb, excluded_dev, cnt,
+                                     off, slot, sids2_dev, bstart2_dev, bsize2_dev, btab2_dev);
+    QS_CHECK_LAUNCH("compact buckets");
     return QS_OK;
 }
 
@@ -706,6 +625,18 @@ int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_
         k_occ_touch<<<qs_blocks(n_pairs, 256), 256, 0, st>>>(pair_key_dev, n_pairs, edges_dev, p, excluded_dev);
     k_occ_finish<<<qs_blocks(n, 256), 256, 0, st>>>(excluded_dev, n, counters_dev);
     QS_CHECK_LAUNCH("occurrence filter");
+    return QS_OK;
+}
+
+int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev, uint64_t n_pairs,
+                        const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p,
+                        uint64_t* out_key_dev, uint32_t* out_sim_dev,
+                        unsigned long long* counter_dev, void* stream) {
+    if (n_pairs == 0) return QS_OK;
+    k_filter_pairs<<<qs_blocks(n_pairs, 256), 256, 0, (cudaStream_t)stream>>>(
+        pair_key_dev, pair_sim_dev, n_pairs, excluded_dev, edges_dev, p, out_key_dev, out_sim_dev,
+        counter_dev);
+    QS_CHECK_LAUNCH("k_filter_pairs");
     return QS_OK;
 }
 

@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(256) k_signatures(
     const uint32_t* __restrict__ bits, uint64_t n, uint32_t K,
     const uint16_t* __restrict__ order, const uint64_t* __restrict__ svals, uint32_t d,
     uint32_t F, uint32_t t, uint32_t kh, uint64_t* __restrict__ sigs,
-    uint64_t* __restrict__ keys, uint32_t* __restrict__ tags, uint32_t* __restrict__ bad) {
+    uint64_t* __restrict__ keys, uint64_t* __restrict__ rkeys, uint32_t* __restrict__ tags,
+    uint32_t* __restrict__ bad) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t words = (d + 31) >> 5;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -154,7 +155,10 @@ __global__ void __launch_bounds__(256) k_signatures(
             }
             if (SEARCH) {
                 const uint64_t key = mix_key(acc);
-                if (i < t) keys[(uint64_t)i * n + row] = key;
+                if (i < t) {
+                    keys[(uint64_t)i * n + row] = key;
+                    rkeys[row * t + i] = key;
+                }
                 const uint32_t tag = (uint32_t)key & 0xFFFFu;
                 uint32_t plane = 0;
 #pragma unroll
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(256) k_signatures(
                     uint32_t word = __ballot_sync(0xffffffffu, (i < t) && ((tag >> b) & 1u));
                     if (lane == (uint32_t)b) plane = word;
                 }
-                if (lane < 16) tags[(row * 16 + lane) * W + wr] = plane;
+                if (lane < 16) tags[(row * W + wr) * 16 + lane] = plane;
             }
         }
         __syncwarp();
@@ -176,8 +180,8 @@ static size_t sig_smem_per_warp(uint32_t d, uint32_t F) {
 
 static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
                              const void* plan, uint32_t d, uint32_t t, uint32_t kh,
-                             uint64_t* sigs, uint64_t* keys, uint32_t* tags, uint32_t* bad,
-                             cudaStream_t st) {
+                             uint64_t* sigs, uint64_t* keys, uint64_t* rkeys, uint32_t* tags,
+                             uint32_t* bad, cudaStream_t st) {
     QS_ARG(K >= 1, "fingerprints must have at least one set bit");
     QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
     QS_ARG(t >= 1 && kh >= 1, "t and k/2 must be >= 1");
@@ -207,10 +211,10 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     unsigned grid = (unsigned)(want < cap ? want : cap);
     if (search)
         k_signatures<true><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
-                                                         sigs, keys, tags, bad);
+                                                         sigs, keys, rkeys, tags, bad);
     else
         k_signatures<false><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
-                                                          sigs, nullptr, nullptr, bad);
+                                                          sigs, nullptr, nullptr, nullptr, bad);
     QS_CHECK_LAUNCH("k_signatures");
     return QS_OK;
 }
@@ -256,15 +260,15 @@ int qs_minmax_signatures(const uint32_t* bits_dev, uint64_t n, uint32_t K, const
                          uint32_t d, uint32_t t, uint32_t k_half, uint64_t* out_dev,
                          uint32_t* bad_dev, void* stream) {
     return launch_signatures(false, bits_dev, n, K, plan_dev, d, t, k_half, out_dev, nullptr,
-                             nullptr, bad_dev, (cudaStream_t)stream);
+                             nullptr, nullptr, bad_dev, (cudaStream_t)stream);
 }
 
 int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K,
                                 const void* plan_dev, uint32_t d, uint32_t t, uint32_t k_half,
-                                uint64_t* sigs_dev, uint64_t* keys_dev, uint32_t* tags_dev,
-                                uint32_t* bad_dev, void* stream) {
+                                uint64_t* sigs_dev, uint64_t* keys_dev, uint64_t* rkeys_dev,
+                                uint32_t* tags_dev, uint32_t* bad_dev, void* stream) {
     return launch_signatures(true, bits_dev, n, K, plan_dev, d, t, k_half, sigs_dev, keys_dev,
-                             tags_dev, bad_dev, (cudaStream_t)stream);
+                             rkeys_dev, tags_dev, bad_dev, (cudaStream_t)stream);
 }
 
 int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,

@@ -138,15 +138,18 @@ def exclusion_windows_for(fps, cfg: SearchConfig) -> int:
 # ---------------------------------------------------------------- device path
 
 class DeviceSearch:
-    """Device buffers + launches of one search over table-major keys/tags.
+    """Device buffers + launches of one search over the search layout.
 
-    keys: (t, n) int64 CUDA tensor (mix64 of the signature words);
-    tags: (n, 16, ceil(t/32)) int32 CUDA tensor.  Also records per-stage CUDA
-    event times when `timing` is set (used by bench.py)."""
+    keys: (t, n) int64 table-major, rkeys: (n, t) int64 row-major (mix64 of
+    the signature words), tags: (n, ceil(t/32), 16) int32 CUDA tensors.
+    Records per-stage CUDA event times when `timing` is set (bench.py)."""
 
-    def __init__(self, keys, tags, n: int, t: int, timing: bool = False):
+    MODE_FULL, MODE_MATCHED, MODE_DISTINCT = 0, 1, 2
+
+    def __init__(self, keys, rkeys, tags, n: int, t: int, timing: bool = False):
         self.torch = nat.torch()
-        self.keys, self.tags, self.n, self.t = keys, tags, n, t
+        self.keys, self.rkeys, self.tags, self.n, self.t = keys, rkeys, tags, n, t
+        self.dev = keys.device
         self.timing = timing
         self.events = []
         self.launches = 0
@@ -163,77 +166,115 @@ class DeviceSearch:
             out[a] = out.get(a, 0.0) + ea.elapsed_time(eb)
         return out
 
+    def _empty(self, nbytes):
+        return self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.dev)
+
     def buckets(self):
         torch, n, t = self.torch, self.n, self.t
         lib = nat.lib()
         self._mark("buckets")
-        self.skeys = torch.empty((t, n), dtype=torch.int64, device=self.keys.device)
-        self.sids = torch.empty((t, n), dtype=torch.int32, device=self.keys.device)
-        ws = torch.empty(int(lib.qs_lsh_bucket_ws_bytes(n, t)), dtype=torch.uint8, device=self.keys.device)
-        nat.call("qs_lsh_build_buckets", nat.ptr(self.keys), n, t, nat.ptr(self.skeys),
+        skeys = torch.empty((t, n), dtype=torch.int64, device=self.dev)
+        self.sids = torch.empty((t, n), dtype=torch.int32, device=self.dev)
+        ws = self._empty(lib.qs_lsh_bucket_ws_bytes(n, t))
+        nat.call("qs_lsh_build_buckets", nat.ptr(self.keys), n, t, nat.ptr(skeys),
                  nat.ptr(self.sids), nat.ptr(ws), ws.numel(), nat.stream())
         del ws
         self.launches += 2 + 3 * 8
         self._mark("list")
-        lws = torch.empty(int(lib.qs_lsh_list_ws_bytes(n, t)), dtype=torch.uint8, device=self.keys.device)
-        counts = torch.zeros(2, dtype=torch.int64, device=self.keys.device)
-        nat.call("qs_lsh_list_buckets", nat.ptr(self.skeys), n, t, None, None, nat.ptr(counts),
+        lws = self._empty(lib.qs_lsh_list_ws_bytes(n, t))
+        counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, None, None, None, nat.ptr(counts),
                  nat.ptr(lws), lws.numel(), nat.stream())
         nb, heads = (int(v) for v in counts.tolist())
         self.nb, self.heads = nb, heads
-        self.bstart = torch.empty(max(nb, 1), dtype=torch.int64, device=self.keys.device)
-        self.bsize = torch.empty(max(nb, 1), dtype=torch.int32, device=self.keys.device)
+        self.bstart = torch.empty(max(nb, 1), dtype=torch.int64, device=self.dev)
+        self.bsize = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
+        self.btab = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         if nb:
-            nat.call("qs_lsh_list_buckets", nat.ptr(self.skeys), n, t, nat.ptr(self.bstart),
-                     nat.ptr(self.bsize), nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
-        self.launches += 4 + 7
-        del self.skeys  # only ids and bucket list are needed downstream
+            nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, nat.ptr(self.bstart),
+                     nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(counts), nat.ptr(lws),
+                     lws.numel(), nat.stream())
+        self.launches += 2 * 4 + 2 * 5 + 1
+        self.full = (self.sids, self.bstart, self.bsize, self.btab, self.nb)
 
-    def pairs(self, m, excl, emask, edges, p, cap=None):
+    def compact(self, emask):
+        """Bucket list with excluded members removed (partitions == 1)."""
+        torch, lib = self.torch, nat.lib()
+        self._mark("compact")
+        nb = self.nb
+        sids2 = torch.empty(max(1, self.n * self.t), dtype=torch.int32, device=self.dev)
+        bstart2 = torch.empty(max(nb, 1), dtype=torch.int64, device=self.dev)
+        bsize2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
+        btab2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
+        counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        ws = self._empty(lib.qs_lsh_compact_ws_bytes(nb))
+        nat.call("qs_lsh_compact_buckets", nat.ptr(self.sids), nat.ptr(self.bstart),
+                 nat.ptr(self.bsize), nat.ptr(self.btab), nb, nat.ptr(emask), nat.ptr(sids2),
+                 nat.ptr(bstart2), nat.ptr(bsize2), nat.ptr(btab2), nat.ptr(counts), nat.ptr(ws),
+                 ws.numel(), nat.stream())
+        self.launches += 2 + 2 * 3
+        nb2 = int(counts[0].item())
+        return (sids2, bstart2, bsize2, btab2, nb2)
+
+    def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None):
         """Enumerate; returns (pair_key int64, pair_sim int32, n_matched, distinct)."""
         torch, lib = self.torch, nat.lib()
-        self._mark("pairs")
-        key = ("cap", self.n, self.t)
-        if cap is None:
+        sids, bstart, bsize, btab, nb = lists if lists is not None else self.full
+        self._mark(("pairs_full", "pairs_matched", "pairs_distinct")[mode])
+        key = ("cap", self.n, self.t, mode)
+        if mode == self.MODE_DISTINCT:
+            cap = 0
+        elif cap is None:
             cap = max(1 << 16, _cap_hint.get(key, 4 * self.n))
-        counters = torch.zeros(2, dtype=torch.int64, device=self.keys.device)
-        ws = torch.empty(int(lib.qs_lsh_pairs_ws_bytes(self.nb)), dtype=torch.uint8, device=self.keys.device)
+        counters = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        ws = self._empty(lib.qs_lsh_pairs_ws_bytes(nb))
         while True:
-            pk = torch.empty(cap, dtype=torch.int64, device=self.keys.device)
-            ps = torch.empty(cap, dtype=torch.int32, device=self.keys.device)
+            pk = torch.empty(max(cap, 1), dtype=torch.int64, device=self.dev)
+            ps = torch.empty(max(cap, 1), dtype=torch.int32, device=self.dev)
             counters.zero_()
-            nat.call("qs_lsh_pairs", nat.ptr(self.sids), nat.ptr(self.bstart), nat.ptr(self.bsize),
-                     self.nb, nat.ptr(self.keys), nat.ptr(self.tags), self.n, self.t, m, excl,
-                     nat.ptr(emask), nat.ptr(edges), p, nat.ptr(pk), nat.ptr(ps), cap,
+            nat.call("qs_lsh_pairs", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize), nat.ptr(btab),
+                     nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n, self.t, m, excl,
+                     nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk), nat.ptr(ps), cap,
                      nat.ptr(counters), nat.ptr(ws), ws.numel(), nat.stream())
-            self.launches += 3
+            self.launches += 5
             distinct, matched = (int(v) for v in counters.tolist())
             if matched <= cap:
                 break
             cap = int(matched * 1.1) + 1024
-            _cap_hint[key] = cap
-        _cap_hint[key] = max(_cap_hint.get(key, 0), int(matched * 1.1) + 1024)
+        if mode != self.MODE_DISTINCT:
+            _cap_hint[key] = max(_cap_hint.get(key, 0), int(matched * 1.1) + 1024)
         return pk[:matched], ps[:matched], matched, distinct
 
     def occurrence(self, pk, ps, matched, threshold, edges, p):
         torch = self.torch
         self._mark("filter")
-        emask = torch.empty(self.n, dtype=torch.uint8, device=self.keys.device)
-        cnt = torch.zeros(1, dtype=torch.int64, device=self.keys.device)
-        ws = torch.empty(self.n, dtype=torch.int32, device=self.keys.device)
+        emask = torch.empty(self.n, dtype=torch.uint8, device=self.dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        ws = torch.empty(self.n, dtype=torch.int32, device=self.dev)
         nat.call("qs_lsh_occurrence_filter", nat.ptr(pk), nat.ptr(ps), matched, self.n,
                  float(threshold), nat.ptr(edges), p, nat.ptr(emask), nat.ptr(cnt), nat.ptr(ws),
                  nat.stream())
         self.launches += 4
         return emask, int(cnt.item())
 
+    def filter_pairs(self, pk, ps, matched, emask, edges, p):
+        torch = self.torch
+        opk = torch.empty(max(matched, 1), dtype=torch.int64, device=self.dev)
+        ops = torch.empty(max(matched, 1), dtype=torch.int32, device=self.dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        nat.call("qs_lsh_filter_pairs", nat.ptr(pk), nat.ptr(ps), matched, nat.ptr(emask),
+                 nat.ptr(edges), p, nat.ptr(opk), nat.ptr(ops), nat.ptr(cnt), nat.stream())
+        self.launches += 1
+        k = int(cnt.item())
+        return opk[:k], ops[:k], k
+
     def bucket_stats(self, emask, edges, p):
         torch = self.torch
         self._mark("stats")
-        hist = torch.zeros(_HIST_LEN, dtype=torch.int64, device=self.keys.device)
+        hist = torch.zeros(_HIST_LEN, dtype=torch.int64, device=self.dev)
         big_cap = max(1024, self.nb // 64)
-        big = torch.empty(big_cap, dtype=torch.int32, device=self.keys.device)
-        out = torch.zeros(4, dtype=torch.int64, device=self.keys.device)
+        big = torch.empty(big_cap, dtype=torch.int32, device=self.dev)
+        out = torch.zeros(4, dtype=torch.int64, device=self.dev)
         nat.call("qs_lsh_bucket_stats", nat.ptr(self.sids), nat.ptr(self.bstart), nat.ptr(self.bsize),
                  self.nb, nat.ptr(emask), nat.ptr(edges), p, nat.ptr(hist), _HIST_LEN, nat.ptr(big),
                  big_cap, nat.ptr(out), nat.stream())
@@ -246,10 +287,9 @@ class DeviceSearch:
     def finalize(self, pk, ps, matched):
         torch, lib = self.torch, nat.lib()
         self._mark("sort")
-        trip = torch.empty(matched * 20, dtype=torch.uint8, device=self.keys.device)
+        trip = torch.empty(matched * 20, dtype=torch.uint8, device=self.dev)
         if matched:
-            ws = torch.empty(int(lib.qs_sort_pairs_ws_bytes(matched)), dtype=torch.uint8,
-                             device=self.keys.device)
+            ws = self._empty(lib.qs_sort_pairs_ws_bytes(matched))
             key_bits = 32 + max(1, int(self.n).bit_length())
             nat.call("qs_lsh_finalize", nat.ptr(pk), nat.ptr(ps), matched, key_bits,
                      nat.ptr(trip), nat.ptr(ws), ws.numel(), nat.stream())
@@ -276,15 +316,15 @@ def _top_mass(hist, big, n_buckets, total):
     return float(acc / total) if total else 0.0
 
 
-def run_search(keys, tags, n: int, t: int, cfg: SearchConfig, exclusion_windows: int,
+def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_windows: int,
                timing: bool = False):
-    """Full search over device keys/tags. Returns (triplets uint8 CUDA tensor of
-    TRIPLET_DTYPE records, SearchStats, DeviceSearch)."""
+    """Full search over the device search layout. Returns (triplets: uint8 CUDA
+    tensor of TRIPLET_DTYPE records, SearchStats, DeviceSearch)."""
     torch = nat.torch()
     stats = SearchStats(n_fingerprints=n)
     bounds = partition_bounds(n, cfg.partitions) if n else []
     stats.partitions = bounds
-    ds = DeviceSearch(keys, tags, n, t, timing=timing)
+    ds = DeviceSearch(keys, rkeys, tags, n, t, timing=timing)
     if n == 0:
         return torch.empty(0, dtype=torch.uint8, device="cuda"), stats, ds
     p = len(bounds)
@@ -294,16 +334,26 @@ def run_search(keys, tags, n: int, t: int, cfg: SearchConfig, exclusion_windows:
     excl = int(exclusion_windows)
     if excl < 0:
         raise ParameterError("exclusion_windows must be >= 0")
+    m = cfg.min_matches
     ds.buckets()
-    emask = None
-    n_ex = 0
-    if cfg.occurrence_threshold is not None:
-        pk, ps, matched, _ = ds.pairs(cfg.min_matches, excl, None, edges, p)
+    emask, n_ex = None, 0
+    if cfg.occurrence_threshold is None:
+        pk, ps, matched, distinct = ds.pairs(ds.MODE_FULL, m, excl, None, edges, p)
+    else:
+        # pass 1: matched pairs (no exclusions yet) -> occurrence filter
+        pk, ps, matched, _ = ds.pairs(ds.MODE_MATCHED, m, excl, None, edges, p)
         emask, n_ex = ds.occurrence(pk, ps, matched, cfg.occurrence_threshold, edges, p)
-        del pk, ps
         if n_ex == 0:
             emask = None
-    pk, ps, matched, distinct = ds.pairs(cfg.min_matches, excl, emask, edges, p)
+            _, _, _, distinct = ds.pairs(ds.MODE_DISTINCT, m, excl, None, edges, p)
+        else:
+            pk, ps, matched = ds.filter_pairs(pk, ps, matched, emask, edges, p)
+            if p == 1:
+                lists = ds.compact(emask)
+                _, _, _, distinct = ds.pairs(ds.MODE_DISTINCT, m, excl, None, edges, p, lists=lists)
+                del lists
+            else:
+                _, _, _, distinct = ds.pairs(ds.MODE_DISTINCT, m, excl, emask, edges, p)
     looks, pieces, mx, hist, big = ds.bucket_stats(emask, edges, p)
     trip = ds.finalize(pk, ps, matched)
     singles = ds.heads - ds.nb
@@ -356,9 +406,11 @@ def search_signatures(sigs, cfg: SearchConfig, exclusion_windows: int = 0):
         sdev = torch.from_numpy(arr.view(np.int64)).to("cuda")
     W = (t + 31) // 32
     keys = torch.empty((t, n), dtype=torch.int64, device=sdev.device)
-    tags = torch.empty((n, 16, W), dtype=torch.int32, device=sdev.device)
-    nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(tags), nat.stream())
-    trip, stats, _ = run_search(keys, tags, n, t, cfg, exclusion_windows)
+    rkeys = torch.empty((n, t), dtype=torch.int64, device=sdev.device)
+    tags = torch.empty((n, W, 16), dtype=torch.int32, device=sdev.device)
+    nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
+             nat.stream())
+    trip, stats, _ = run_search(keys, rkeys, tags, n, t, cfg, exclusion_windows)
     if on_device:
         return trip, stats
     return trip.cpu().numpy().view(TRIPLET_DTYPE), stats
@@ -373,11 +425,13 @@ def signatures_for_search(bits, mapping: HashMapping):
     W = (t + 31) // 32
     _, plan = mapping.device_plan()
     keys = torch.empty((t, n), dtype=torch.int64, device=bits.device)
-    tags = torch.empty((n, 16, W), dtype=torch.int32, device=bits.device)
+    rkeys = torch.empty((n, t), dtype=torch.int64, device=bits.device)
+    tags = torch.empty((n, W, 16), dtype=torch.int32, device=bits.device)
     bad = torch.zeros(1, dtype=torch.int32, device=bits.device)
     nat.call("qs_minmax_signatures_search", nat.ptr(bits), n, K, nat.ptr(plan), mapping.d, t,
-             mapping.k_half, None, nat.ptr(keys), nat.ptr(tags), nat.ptr(bad), nat.stream())
-    return keys, tags, bad
+             mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags), nat.ptr(bad),
+             nat.stream())
+    return keys, rkeys, tags, bad
 
 
 def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = None,
@@ -416,10 +470,10 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
     if n == 0:
         empty = _empty_triplets() if not on_device else torch.empty(0, dtype=torch.uint8, device="cuda")
         return empty, SearchStats(n_fingerprints=0), mapping
-    keys, tags, bad = signatures_for_search(bdev, mapping)
+    keys, rkeys, tags, bad = signatures_for_search(bdev, mapping)
     if on_device and int(bad.item()):
         raise ParameterError("fingerprint bit index out of range for mapping")
-    trip, stats, _ = run_search(keys, tags, n, cfg.tables, cfg, excl)
+    trip, stats, _ = run_search(keys, rkeys, tags, n, cfg.tables, cfg, excl)
     if on_device:
         return trip, stats, mapping
     return trip.cpu().numpy().view(TRIPLET_DTYPE), stats, mapping
