@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--group-frac", type=float, default=1 / 400, help="noise-group density (design experiments)")
     return ap.parse_args()
 
 
@@ -189,7 +190,7 @@ def run_ours(args):
 
     n = args.n
     occ = args.occ if args.occ > 0 else None
-    bits, _ = workloads.cfg1_bits_torch(n=n, seed=1 + rank, device=dev)
+    bits, _ = workloads.cfg1_bits_torch(n=n, seed=1 + rank, device=dev, group_frac=args.group_frac)
     torch.cuda.synchronize()
     mapping = mh.gen_hash_mapping(4096, 100, 4, 0)
     mapping.device_plan()

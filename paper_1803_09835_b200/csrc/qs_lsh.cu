@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
                 uint32_t word = __ballot_sync(0xffffffffu, (i < t) && ((tag >> b) & 1u));
                 if (lane == (uint32_t)b) plane = word;
             }
-            if (lane < 16) tags[(row * W + wr) * 16 + lane] = plane;
+            if (lane < 16) tags[((uint64_t)(lane >> 3) * n + row) * W * 8 + wr * 8 + (lane & 7)] = plane;
         }
     }
 }

@@ -2,43 +2,131 @@
 //
 // Replaces the reference's per-query gather + (q << 32 | c) key materialisation
 // + sort + run-length count (lsh_search.py:175-219) and the >= m threshold
-// (:261, :281).  Work unit: a 32-member chunk of one bucket; lane i holds
-// member a_i's bit-sliced tag planes in registers, the bucket's members are
-// staged 32 at a time in shared memory (cp.async, double buffered: the next
-// batch streams in while the current one is compared) and every lane compares
-// its row with each staged row (broadcast shared-memory reads + LOP3).
+// (:261, :281).
+//
+// Work decomposition (persistent CTAs, warp-specialised producer/consumer):
+//   * a work ITEM is a TILE of consecutive buckets of size <= L (<= 2L
+//     members) or one (I, J) segment pair of a bigger bucket (L-member
+//     segments); items are listed by a planning pass;
+//   * one PRODUCER warp per CTA stages item k+1's member ids and bit-sliced
+//     tag rows into the other half of a double-buffered shared-memory area
+//     (cp.async, completion tracked by an mbarrier) while the CONSUMER warps
+//     compare item k: each consumer warp takes 32-row x 64-row chunks, lane i
+//     holds member a_i's tag planes in registers and compares them with the
+//     later rows (broadcast shared-memory reads, 1 LOP3 per plane-word);
+//   * consumers never wait for each other: a warp that runs out of chunks
+//     releases the buffer (mbarrier arrive) and moves on to the next item, so
+//     load latency and tail imbalance are both hidden.
 //
 // Exactness: each unordered pair is handled only in the bucket of its FIRST
 // colliding table.  Tag-plane masks over-approximate the set of colliding
 // tables (tags: false positives only), so every table a decision depends on
 // is confirmed on the 64-bit keys (rkeys, row-major).  Confirmations are rare
 // and divergent, so candidates are queued per warp in shared memory and
-// drained 32 at a time with one candidate per lane (convergent, 32 independent
-// key loads in flight).
+// drained 32 at a time with one candidate per lane.
+//
+// Tag layout: tags[2][n][W][8] uint32 (plane groups 0-7 / 8-15), W = ceil(t/32).
 //
 // Modes (warp-uniform, compile time):
 //   FULL      distinct-pair count + emission of sim >= m (no occurrence filter)
-//   MATCHED   emission only (occurrence-filter pass 1): screen on 8 planes
+//   MATCHED   emission only (occurrence-filter pass 1): screen on planes 0-7
 //   DISTINCT  distinct-pair count only (pass 2 after the filter)
 #include "qs_lsh.cuh"
 
 namespace qs {
 
-constexpr uint32_t GRAB = 8;
 constexpr int QCAP = 64;
+// Occupancy configuration (measured on B200 at cfg1): 4 CTAs per
+// SM, each 1 producer + 3 consumer warps with two 22 KB staged items.
+#ifndef QS_CWARPS
+#define QS_CWARPS 3
+#define QS_BUFKB 22
+#define QS_MINB 4
+#endif
+#ifndef QS_NBUF
+#define QS_NBUF 2
+#endif
+constexpr int NBUF = QS_NBUF;          // staged items in flight per CTA (ring)
+constexpr int CWARPS = QS_CWARPS;      // consumer warps per CTA (+1 producer warp)
+constexpr int PTHREADS = (CWARPS + 1) * 32;
+constexpr uint32_t BPIECE = 64;        // B rows per chunk
+constexpr uint32_t NCH_DONE = 0xFFFFFFFFu;
 enum { MODE_FULL = 0, MODE_MATCHED = 1, MODE_DISTINCT = 2 };
 
+#ifdef QS_PROF  // design instrumentation (not built by default)
+__device__ unsigned long long g_prof[8];
+#define PROF_DECL unsigned long long pr_acc[4] = {0, 0, 0, 0}; long long pr_t = 0;
+#define PROF_START pr_t = clock64();
+#define PROF_STOP(i) pr_acc[i] += (unsigned long long)(clock64() - pr_t);
+#define PROF_FLUSH(base) if (lane == 0) for (int _i = 0; _i < 4; ++_i) atomicAdd(&g_prof[base + _i], pr_acc[_i]);
+#else
+#define PROF_DECL
+#define PROF_START
+#define PROF_STOP(i)
+#define PROF_FLUSH(base)
+#endif
+
 template <int W, int MODE>
-struct PairCfg {
-    static constexpr int NP = MODE == MODE_MATCHED ? 8 : 16;    // planes staged / in registers
-    static constexpr int WARPS = MODE == MODE_MATCHED ? 8 : 4;  // warps per CTA
-    static constexpr int ROW = W * NP;                          // u32 per staged row
-    // per-warp shared memory (u32 units): 2 row buffers + 2 id buffers + queue
+struct TileCfg {
+    static constexpr int NP = MODE == MODE_MATCHED ? 8 : 16;  // planes staged / in registers
+    static constexpr int ROW = W * NP;                        // u32 per staged row
+    static constexpr int ROWP = ROW + 4;                      // padded stride: row-parallel
+                                                              // 16-byte loads are conflict-free
+    static constexpr int CAP = (QS_BUFKB * 1024) / (ROWP * 4);  // rows per buffer
+    static constexpr int L = CAP / 2;                         // small-bucket / segment limit
+    static constexpr int MAXCH = L + (L / 32 + 1) * (L / 64 + 2) + 16;
     static constexpr int QWORDS = QCAP * (3 + W);
-    static constexpr int PER_WARP = 2 * 32 * ROW + 2 * 32 + QWORDS;
+    // per buffer: rows, ids, chunk descriptors
+    static constexpr size_t IDS_BYTES = ((size_t)CAP * 4 + 15) & ~(size_t)15;
+    static constexpr size_t BUF =
+        (((size_t)CAP * ROWP * 4 + IDS_BYTES + (size_t)MAXCH * 8) + 127) & ~(size_t)127;
+    static constexpr size_t SMEM = NBUF * BUF + (size_t)CWARPS * QWORDS * 4 + 128;
 };
 
-// AND over np planes of ~(A ^ B) for 32-table word w; R is a staged row with NP planes/word
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
+// AND over np planes of ~(A ^ B) for 32-table word w of the staged row R
+// (uniform across the warp: broadcast shared-memory reads, immediate offsets).
 template <int W, int NP>
 __device__ __forceinline__ uint32_t pmask(const uint32_t (&A)[W][NP], const uint32_t* R, int w,
                                           int np) {
@@ -86,15 +174,7 @@ __device__ __forceinline__ uint32_t confirm(const uint64_t* __restrict__ rkeys, 
     return hits;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// Queue entry flags (bits 8.. of qt; bits 0..7 = table & 0xFF, table >> 8 kept in bits 16..)
+// Queue entry flags (bits 0..7 = table & 0xFF, bits 16.. = table >> 8)
 constexpr uint32_t QF_COUNT = 1u << 8;     // needs the confirmed count (emit if >= m)
 constexpr uint32_t QF_DISTINCT = 1u << 9;  // count as a distinct pair when first
 
@@ -151,86 +231,284 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
     __syncwarp();
 }
 
+// chunk descriptor: x = abase | bbeg << 16; y = bend | acnt << 16 | tri << 22 | table << 23
+__device__ __forceinline__ uint2 make_chunk(uint32_t abase, uint32_t acnt, uint32_t bbeg,
+                                            uint32_t bend, bool tri, uint32_t table) {
+    return make_uint2(abase | (bbeg << 16),
+                      bend | (acnt << 16) | ((tri ? 1u : 0u) << 22) | (table << 23));
+}
+__device__ __forceinline__ uint32_t n_pieces(uint32_t bb, uint32_t be) {
+    return be > bb ? (be - bb + BPIECE - 1) / BPIECE : 0;
+}
+// all chunks of the rows [off, off + s) of one bucket (pairs j > i)
+__device__ __forceinline__ uint32_t count_chunks_tri(uint32_t s) {
+    uint32_t n = 0;
+    for (uint32_t c = 0; c * 32 < s; ++c) n += n_pieces(c * 32 + 1, s);
+    return n;
+}
+__device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, uint32_t off,
+                                                uint32_t s, uint32_t table) {
+    for (uint32_t c = 0; c * 32 < s; ++c) {
+        const uint32_t ab = off + c * 32, acnt = min(32u, s - c * 32);
+        const uint32_t np = n_pieces(c * 32 + 1, s);
+        for (uint32_t k = 0; k < np; ++k) {
+            const uint32_t b0 = ab + 1 + k * BPIECE;
+            chunks[base++] = make_chunk(ab, acnt, b0, min(off + s, b0 + BPIECE), true, table);
+        }
+    }
+}
+
+template <int W, int NP>
+__device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const uint32_t* __restrict__ tags,
+                                          uint64_t n, uint32_t id) {
+    uint4* dst = (uint4*)(rows + pos * (W * NP + 4));
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+#pragma unroll
+        for (int qq = 0; qq < NP / 4; ++qq) {
+            const uint32_t grp = qq >> 1;  // plane group (0: planes 0-7, 1: planes 8-15)
+            cp_async16(dst + (w * (NP / 4) + qq),
+                       tags + ((uint64_t)grp * n + id) * W * 8 + w * 8 + (qq & 1) * 4);
+        }
+}
+
+struct Plan {
+    const uint64_t* mpre;        // exclusive prefix of small-bucket sizes (nb + 1)
+    const uint64_t* tile_first;  // first bucket of each tile (n_tiles + 1)
+    const uint64_t* bigitems;    // (bucket << 24) | (I << 12) | J per big item (if totals[5])
+    const uint64_t* bigb;        // big bucket indices
+    const uint64_t* bigoff;      // exclusive prefix of items per big bucket
+    const uint64_t* totals;      // [0] small members, [1] n_big, [2] n_tiles, [3] n_bigitems,
+                                 // [4] max segments per bucket, [5] item table valid
+};
+
 template <int W, int MODE, bool HAS_E>
-__global__ void __launch_bounds__(PairCfg<W, MODE>::WARPS * 32) k_pairs(
+__global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
     const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
-    const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
-    const uint64_t* __restrict__ chunk_off, uint64_t nb, const uint64_t* __restrict__ rkeys,
-    const uint32_t* __restrict__ tags, uint32_t t, uint32_t m, uint64_t excl,
-    const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges, uint32_t p,
-    uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
+    const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab, Plan plan,
+    const uint64_t* __restrict__ rkeys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
+    uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges,
+    uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
     unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work) {
-    using C = PairCfg<W, MODE>;
+    using C = TileCfg<W, MODE>;
     constexpr int NP = C::NP;
-    extern __shared__ __align__(16) uint32_t psm[];
+    constexpr uint32_t L = C::L;
+    extern __shared__ __align__(128) unsigned char psm[];
+    __shared__ __align__(8) uint64_t full_bar[NBUF], empty_bar[NBUF];
+    __shared__ uint32_t s_nch[NBUF], s_next[NBUF];
+    // producer scratch: tile bucket metadata, small-bucket offsets / member-list starts
+    __shared__ uint64_t m_mpre[L + 1], m_bstart[L], p_st[L];
+    __shared__ uint32_t m_bsize[L], m_btab[L], p_off[L + 1];
+    // buffer b: rows | ids | chunk descriptors
+    auto rowsb = [&](int b) { return (uint32_t*)(psm + b * C::BUF); };
+    auto idsb = [&](int b) { return (uint32_t*)(psm + b * C::BUF + (size_t)C::CAP * C::ROWP * 4); };
+    auto chb = [&](int b) {
+        return (uint2*)(psm + b * C::BUF + (size_t)C::CAP * C::ROWP * 4 + C::IDS_BYTES);
+    };
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* wbase = psm + warp * C::PER_WARP;
-    uint32_t* rows0 = wbase;                       // [2][32][ROW]
-    uint32_t* rid0 = wbase + 2 * 32 * C::ROW;      // [2][32]
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBUF; ++i) {
+            mbar_init(&full_bar[i], 64);
+            mbar_init(&empty_bar[i], CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t n_tiles = plan.totals[2], n_items = n_tiles + plan.totals[3];
+    const bool use_table = plan.totals[5] != 0;
+
+    if (warp == CWARPS) {
+        // ================================================= producer warp
+        PROF_DECL
+        unsigned long long item_next = 0;
+        if (lane == 0) item_next = atomicAdd(work, 1ULL);
+        for (uint32_t k = 0;; ++k) {
+            const int b = k % NBUF;
+            // the next grab is issued one item ahead so its latency overlaps this item
+            unsigned long long item = __shfl_sync(0xffffffffu, item_next, 0);
+            if (lane == 0 && item < n_items) item_next = atomicAdd(work, 1ULL);
+            PROF_START
+            if (k >= NBUF) mbar_wait(&empty_bar[b], ((k / NBUF) - 1) & 1);
+            PROF_STOP(0)
+            PROF_START
+            uint32_t* rows = rowsb(b);
+            uint32_t* ids = idsb(b);
+            uint2* chunks = chb(b);
+            if (item >= n_items) {
+                if (lane == 0) s_nch[b] = NCH_DONE;
+                mbar_arrive_cp_async(&full_bar[b]);
+                mbar_arrive(&full_bar[b]);
+                break;
+            }
+            if (lane == 0) {
+                s_nch[b] = 0;
+                s_next[b] = 0;
+            }
+            __syncwarp();
+            if (item < n_tiles) {
+                const uint64_t b0 = plan.tile_first[item], b1 = plan.tile_first[item + 1];
+                const uint32_t cnt = (uint32_t)(b1 - b0);
+                // the tile's bucket metadata -> shared memory in one async round trip
+                for (uint32_t i = lane; i <= cnt; i += 32) {
+                    cp_async8(m_mpre + i, plan.mpre + b0 + i);
+                    if (i < cnt) {
+                        cp_async4(m_bsize + i, bsize + b0 + i);
+                        cp_async8(m_bstart + i, bstart + b0 + i);
+                        cp_async4(m_btab + i, btab + b0 + i);
+                    }
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                const uint64_t mbase = m_mpre[0];
+                // small buckets of the tile (order-preserving compaction, one lane per
+                // bucket) and their chunk descriptors
+                const uint32_t lt = (1u << lane) - 1u;
+                uint32_t nsb = 0;
+                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+                    const uint32_t i = i0 + lane;
+                    const uint32_t s = i < cnt ? m_bsize[i] : 0u;
+                    const bool small = i < cnt && s <= L;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, small);
+                    if (small) {
+                        const uint32_t kk = nsb + __popc(bal & lt);
+                        const uint32_t off = (uint32_t)(m_mpre[i] - mbase);
+                        p_off[kk] = off;
+                        p_st[kk] = m_bstart[i];
+                        const uint32_t cb = atomicAdd(&s_nch[b], count_chunks_tri(s));
+                        emit_chunks_tri(chunks, cb, off, s, m_btab[i]);
+                    }
+                    nsb += __popc(bal);
+                }
+                const uint32_t tot = (uint32_t)(m_mpre[cnt] - mbase);
+                if (lane == 0) p_off[nsb] = tot;
+                __syncwarp();
+                // member ids, one lane per member (bucket found by binary search)
+                for (uint32_t r = lane; r < tot; r += 32) {
+                    uint32_t lo = 0, hi = nsb;
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (p_off[mid] <= r) lo = mid;
+                        else hi = mid;
+                    }
+                    cp_async4(ids + r, sids + p_st[lo] + (r - p_off[lo]));
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                for (uint32_t r = lane; r < tot; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
+            } else {
+                uint64_t bk;
+                uint32_t I, J;
+                if (use_table) {
+                    const uint64_t e = plan.bigitems[item - n_tiles];
+                    bk = e >> 24;
+                    I = (uint32_t)(e >> 12) & 0xFFFu;
+                    J = (uint32_t)e & 0xFFFu;
+                } else {  // giant buckets: decode (bucket, I, J) from the item prefix
+                    const uint64_t idx = item - n_tiles;
+                    uint64_t lo = 0, hi = plan.totals[1];
+                    while (hi - lo > 1) {
+                        const uint64_t mid = (lo + hi) >> 1;
+                        if (plan.bigoff[mid] <= idx) lo = mid;
+                        else hi = mid;
+                    }
+                    bk = plan.bigb[lo];
+                    const uint64_t nseg = (bsize[bk] + L - 1) / L;
+                    uint64_t rem = idx - plan.bigoff[lo], ii = 0;
+                    while (rem >= nseg - ii) {
+                        rem -= nseg - ii;
+                        ++ii;
+                    }
+                    I = (uint32_t)ii;
+                    J = (uint32_t)(ii + rem);
+                }
+                const uint32_t s = bsize[bk];
+                const uint64_t st = bstart[bk];
+                const uint32_t i0 = I * L, nI = min(L, s - i0);
+                const uint32_t j0 = J * L, nJ = (J == I) ? 0 : min(L, s - j0);
+                for (uint32_t r = lane; r < nI + nJ; r += 32)
+                    cp_async4(ids + r, sids + st + (r < nI ? i0 + r : j0 + (r - nI)));
+                if (lane == 0) {
+                    const uint32_t table = btab[bk];
+                    uint32_t cbase = 0;
+                    if (J == I) {
+                        emit_chunks_tri(chunks, 0, 0, nI, table);
+                        cbase = count_chunks_tri(nI);
+                    } else {
+                        for (uint32_t c = 0; c * 32 < nI; ++c) {
+                            const uint32_t np = n_pieces(nI, nI + nJ);
+                            for (uint32_t kk = 0; kk < np; ++kk) {
+                                const uint32_t bb = nI + kk * BPIECE;
+                                chunks[cbase++] = make_chunk(c * 32, min(32u, nI - c * 32), bb,
+                                                             min(nI + nJ, bb + BPIECE), false, table);
+                            }
+                        }
+                    }
+                    s_nch[b] = cbase;
+                }
+                cp_async_wait_all();
+                __syncwarp();
+                for (uint32_t r = lane; r < nI + nJ; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
+            }
+            __syncwarp();
+            mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
+            mbar_arrive(&full_bar[b]);           // releases ids / descriptors / counters
+            PROF_STOP(1)
+        }
+        PROF_FLUSH(0)
+        return;
+    }
+
+    // ===================================================== consumer warps
+    PROF_DECL
+    uint32_t* qbase = (uint32_t*)(psm + NBUF * C::BUF) + warp * C::QWORDS;
     Queue q;
-    q.qa = rid0 + 64;
+    q.qa = qbase;
     q.qb = q.qa + QCAP;
     q.qt = q.qb + QCAP;
     q.qm = q.qt + QCAP;
-    uint32_t qhead = 0, qn = 0;  // warp-uniform ring state
-    const uint64_t total_chunks = chunk_off[nb];
+    uint32_t qhead = 0, qn = 0;
     const uint32_t last_mask = (t & 31) ? ((1u << (t & 31)) - 1u) : 0xFFFFFFFFu;
     const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long distinct = 0;
 
-    while (true) {
-        unsigned long long g0 = 0;
-        if (lane == 0) g0 = atomicAdd(work, (unsigned long long)GRAB);
-        g0 = __shfl_sync(0xffffffffu, g0, 0);
-        if (g0 >= total_chunks) break;
-        const uint64_t g1 = min((uint64_t)g0 + GRAB, total_chunks);
-        uint64_t lo = 0, hi = nb;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (chunk_off[mid] <= g0) lo = mid;
-            else hi = mid;
-        }
-        uint64_t b = lo;
-        for (uint64_t g = g0; g < g1; ++g) {
-            while (chunk_off[b + 1] <= g) ++b;
-            const uint32_t c = (uint32_t)(g - chunk_off[b]);
-            const uint64_t st = bstart[b];
-            const uint32_t s = bsize[b];
-            const uint32_t table = btab[b];
+    for (uint32_t k = 0;; ++k) {
+        const int bsel = k % NBUF;
+        PROF_START
+        mbar_wait(&full_bar[bsel], (k / NBUF) & 1);
+        PROF_STOP(0)
+        PROF_START
+        const uint32_t nch = s_nch[bsel];
+        if (nch == NCH_DONE) break;
+        const uint32_t* rows = rowsb(bsel);
+        const uint32_t* ids = idsb(bsel);
+        const uint2* chunks = chb(bsel);
+        while (true) {
+            uint32_t ci = 0;
+            if (lane == 0) ci = atomicAdd(&s_next[bsel], 1u);
+            ci = __shfl_sync(0xffffffffu, ci, 0);
+            if (ci >= nch) break;
+            const uint2 d = chunks[ci];
+            const uint32_t abase = d.x & 0xFFFFu, bbeg = d.x >> 16;
+            const uint32_t bend = d.y & 0xFFFFu, acnt = (d.y >> 16) & 63u;
+            const bool tri = (d.y >> 22) & 1u;
+            const uint32_t table = d.y >> 23;
             const int wt = (int)(table >> 5);
             const uint32_t bt = table & 31, low = (1u << bt) - 1u;
             const uint32_t tflag = (table & 0xFFu) | ((table >> 8) << 16);
-            const uint32_t i = c * 32 + lane;
-            const bool active = i < s;
-            const uint32_t a = active ? sids[st + i] : 0;
-            // first staged batch (cp.async) overlaps the register loads of row a
-            uint32_t jb = c * 32;
-            int buf = 0;
-            {
-                const uint32_t jj = jb + lane;
-                const uint32_t bid = jj < s ? sids[st + jj] : 0;
-                rid0[lane] = bid;
-                if (jj < s) {
-                    uint32_t* dst = rows0 + lane * C::ROW;
-#pragma unroll
-                    for (int w = 0; w < W; ++w)
-#pragma unroll
-                        for (int qq = 0; qq < NP / 4; ++qq)
-                            cp_async16(dst + w * NP + qq * 4, tags + ((uint64_t)bid * W + w) * 16 + qq * 4);
-                }
-                cp_async_commit();
-            }
-            uint32_t nxt = (jb + 32 + lane < s) ? sids[st + jb + 32 + lane] : 0;
+            const bool active = lane < acnt;
+            const uint32_t apos = abase + (active ? lane : 0);
+            const uint32_t a = ids[apos];
             uint32_t A[W][NP];
+            {
+                const uint4* src = (const uint4*)(rows + apos * C::ROWP);
 #pragma unroll
-            for (int w = 0; w < W; ++w) {
-                const uint4* src = (const uint4*)(tags + ((uint64_t)a * W + w) * 16);
+                for (int w = 0; w < W; ++w)
 #pragma unroll
-                for (int qq = 0; qq < NP / 4; ++qq) {
-                    const uint4 v = active ? __ldg(src + qq) : make_uint4(0, 0, 0, 0);
-                    A[w][qq * 4 + 0] = v.x; A[w][qq * 4 + 1] = v.y;
-                    A[w][qq * 4 + 2] = v.z; A[w][qq * 4 + 3] = v.w;
-                }
+                    for (int qq = 0; qq < NP / 4; ++qq) {
+                        const uint4 v = src[w * (NP / 4) + qq];
+                        A[w][qq * 4 + 0] = v.x; A[w][qq * 4 + 1] = v.y;
+                        A[w][qq * 4 + 2] = v.z; A[w][qq * 4 + 3] = v.w;
+                    }
             }
             bool a_ok = active;
             uint32_t a_part = 0;
@@ -238,131 +516,183 @@ __global__ void __launch_bounds__(PairCfg<W, MODE>::WARPS * 32) k_pairs(
                 a_ok = emask[a] == 0;
                 a_part = p > 1 ? part_of(edges, p, a) : 0;
             }
-            for (; jb < s; jb += 32) {
-                const bool more = jb + 32 < s;
-                if (more) {
-                    uint32_t* rows_n = rows0 + (buf ^ 1) * 32 * C::ROW;
-                    rid0[(buf ^ 1) * 32 + lane] = nxt;
-                    if (jb + 32 + lane < s) {
-                        uint32_t* dst = rows_n + lane * C::ROW;
-#pragma unroll
-                        for (int w = 0; w < W; ++w)
-#pragma unroll
-                            for (int qq = 0; qq < NP / 4; ++qq)
-                                cp_async16(dst + w * NP + qq * 4,
-                                           tags + ((uint64_t)nxt * W + w) * 16 + qq * 4);
-                    }
-                    cp_async_commit();
-                    nxt = (jb + 64 + lane < s) ? sids[st + jb + 64 + lane] : 0;
-                    cp_async_wait<1>();
-                } else {
-                    cp_async_wait<0>();
-                }
-                __syncwarp();
-                const uint32_t* rows = rows0 + buf * 32 * C::ROW;
-                const uint32_t* rid = rid0 + buf * 32;
-                const uint32_t un = min(32u, s - jb);
-                const uint32_t u0 = (jb == c * 32) ? 1 : 0;
-                for (uint32_t u = u0; u < un; ++u) {
-                    const uint32_t bid = rid[u];
-                    bool valid = a_ok && (jb + u > i);
-                    const uint64_t dt = (uint64_t)bid - a;  // ids ascend within a bucket
-                    valid = valid && dt > excl;
-                    if (HAS_E && valid && emask[bid] && (p <= 1 || part_of(edges, p, bid) == a_part))
+            const uint32_t u_lo = tri ? apos + 1 : bbeg;  // pairs j > i within a bucket
+            const bool excl_on = excl > 0;
+            const uint32_t* R = rows + bbeg * C::ROWP;
+            for (uint32_t u = bbeg; u < bend; ++u, R += C::ROWP) {
+                bool valid = a_ok && u >= u_lo;
+                if (excl_on || HAS_E) {
+                    const uint32_t bid = ids[u];
+                    valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend within a bucket
+                    if (HAS_E && valid && emask[bid] &&
+                        (p <= 1 || part_of(edges, p, bid) == a_part))
                         valid = false;
-                    bool slow = false;
-                    uint32_t qmask[W];
+                }
+                bool slow = false;
+                uint32_t qmask[W];
+                uint32_t flags = tflag;
+                // masks are computed for every lane (no divergence); invalid lanes drop them
+                if (MODE == MODE_MATCHED) {
+                    uint32_t cnt = 0;
 #pragma unroll
-                    for (int w = 0; w < W; ++w) qmask[w] = 0;
-                    uint32_t flags = tflag;
-                    if (valid) {
-                        const uint32_t* R = rows + u * C::ROW;
-                        if (MODE == MODE_MATCHED) {
-                            uint32_t cnt = 0;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) {
-                                uint32_t s8 = pmask<W, NP>(A, R, w, 8);
-                                if (w == W - 1) s8 &= last_mask;
-                                qmask[w] = s8;
-                                cnt += __popc(s8);
-                            }
-                            slow = cnt >= m;
-                            flags |= QF_COUNT;
-                        } else {
-                            uint32_t early = 0, cnt = 0;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) {
-                                uint32_t x;
-                                if (w <= wt) {
-                                    x = pmask<W, NP>(A, R, w, 16);
-                                    if (w == W - 1) x &= last_mask;
-                                    early |= (w < wt) ? x : (x & low);
-                                    if (w == wt) cnt += __popc(x & ~low);
-                                } else if (MODE == MODE_FULL) {
-                                    x = pmask<W, NP>(A, R, w, 8);
-                                    if (w == W - 1) x &= last_mask;
-                                    cnt += __popc(x);
-                                } else {
-                                    x = 0;
-                                }
-                                qmask[w] = x;
-                            }
-                            const bool need_count = (MODE == MODE_FULL) && cnt >= m;
-                            if (early) {
-                                slow = true;  // first-table rule needs confirmation
-                                flags |= QF_DISTINCT | (need_count ? QF_COUNT : 0u);
-                            } else {
-                                ++distinct;
-                                if (need_count) {
-                                    slow = true;
-                                    flags |= QF_COUNT;
-                                }
-                            }
-                        }
+                    for (int w = 0; w < W; ++w) {
+                        uint32_t s8 = pmask<W, NP>(A, R, w, 8);
+                        if (w == W - 1) s8 &= last_mask;
+                        qmask[w] = s8;
+                        cnt += __popc(s8);
                     }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, slow);
-                    if (bal) {
-                        if (slow) {
-                            const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
-                            q.qa[e] = a;
-                            q.qb[e] = bid;
-                            q.qt[e] = flags;
+                    slow = valid && cnt >= m;
+                    flags |= QF_COUNT;
+                } else {
+                    uint32_t early = 0, cnt = 0;
 #pragma unroll
-                            for (int w = 0; w < W; ++w) q.qm[e * W + w] = qmask[w];
+                    for (int w = 0; w < W; ++w) {
+                        uint32_t x = 0;
+                        if (w <= wt) {
+                            x = pmask<W, NP>(A, R, w, 16);
+                            if (w == W - 1) x &= last_mask;
+                            early |= (w < wt) ? x : (x & low);
+                            if (w == wt) cnt += __popc(x & ~low);
+                        } else if (MODE == MODE_FULL) {
+                            x = pmask<W, NP>(A, R, w, 8);
+                            if (w == W - 1) x &= last_mask;
+                            cnt += __popc(x);
                         }
-                        qn += __popc(bal);
-                        if (qn >= 32) {
-                            __syncwarp();
-                            drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, cap,
-                                     counters, distinct);
-                            qhead = (qhead + 32) & (QCAP - 1);
-                            qn -= 32;
+                        qmask[w] = x;
+                    }
+                    const bool need_count = (MODE == MODE_FULL) && cnt >= m;
+                    if (valid) {
+                        if (early) {
+                            slow = true;  // first-table rule needs confirmation
+                            flags |= QF_DISTINCT | (need_count ? QF_COUNT : 0u);
+                        } else {
+                            ++distinct;
+                            if (need_count) {
+                                slow = true;
+                                flags |= QF_COUNT;
+                            }
                         }
                     }
                 }
-                __syncwarp();
-                buf ^= 1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, slow);
+                if (bal) {
+                    if (slow) {
+                        const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
+                        q.qa[e] = a;
+                        q.qb[e] = ids[u];
+                        q.qt[e] = flags;
+#pragma unroll
+                        for (int w = 0; w < W; ++w) q.qm[e * W + w] = qmask[w];
+                    }
+                    qn += __popc(bal);
+                    if (qn >= 32) {
+                        __syncwarp();
+                        PROF_STOP(1)
+                        PROF_START
+                        drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, cap, counters,
+                                 distinct);
+                        PROF_STOP(2)
+                        PROF_START
+                        qhead = (qhead + 32) & (QCAP - 1);
+                        qn -= 32;
+                    }
+                }
             }
         }
+        __syncwarp();
+        PROF_STOP(1)
+        if (lane == 0) mbar_arrive(&empty_bar[bsel]);
     }
     __syncwarp();
     if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, cap, counters, distinct);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
     if (lane == 0 && distinct) atomicAdd(counters + 0, distinct);
+    PROF_FLUSH(4)
 }
 
-// Generic path for t > 128 (any mode, no register caching): exact masks from
-// the tag planes in global memory, confirmed on the keys.
-__device__ __forceinline__ uint32_t gmask16(const uint32_t* __restrict__ tags, uint32_t W,
-                                            uint32_t a, uint32_t b, int w) {
-    const uint4* pa = (const uint4*)(tags + ((uint64_t)a * W + w) * 16);
-    const uint4* pb = (const uint4*)(tags + ((uint64_t)b * W + w) * 16);
+// --------------------------------------------------------------- planning
+__global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, uint64_t nb, uint32_t L,
+                             uint64_t* __restrict__ small, uint64_t* __restrict__ bigflag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nb;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = i < nb ? bsize[i] : 0;
+        small[i] = (i < nb && s <= L) ? s : 0;
+        bigflag[i] = (i < nb && s > L) ? 1 : 0;
+    }
+}
+
+// per big bucket k: its item count (scan input) and bucket index
+__global__ void k_plan_big(const uint32_t* __restrict__ bsize, uint64_t nb, uint32_t L,
+                           const uint64_t* __restrict__ bigpos, uint64_t* __restrict__ bigb,
+                           uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = bsize[i];
+        if (s <= L) continue;
+        const uint64_t k = bigpos[i];
+        const uint64_t nseg = (s + L - 1) / L;
+        bigb[k] = i;
+        bigcnt[k] = nseg * (nseg + 1) / 2;
+        atomicMax(maxnseg, (unsigned long long)nseg);
+    }
+}
+
+__global__ void k_plan_bigitems(const uint32_t* __restrict__ bsize, const uint64_t* __restrict__ bigb,
+                                const uint64_t* __restrict__ bigoff, const uint64_t* __restrict__ totals,
+                                uint32_t L, uint64_t* __restrict__ items, uint64_t items_cap) {
+    const uint64_t nbig = totals[1];
+    if (totals[3] > items_cap || totals[4] > 4095) return;  // decoded on the fly instead
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nbig;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = bigb[k];
+        const uint32_t nseg = (bsize[b] + L - 1) / L;
+        uint64_t o = bigoff[k];
+        for (uint32_t I = 0; I < nseg; ++I)
+            for (uint32_t J = I; J < nseg; ++J) items[o++] = (b << 24) | ((uint64_t)I << 12) | J;
+    }
+}
+
+// totals[2] = n_tiles; tile_first[k] = lower_bound(mpre, k * L), tile_first[n_tiles] = nb
+__global__ void k_plan_tiles(const uint64_t* __restrict__ mpre, uint64_t nb, uint32_t L,
+                             uint64_t* __restrict__ totals, const uint64_t* __restrict__ bigoff,
+                             uint64_t* __restrict__ tile_first, uint64_t items_cap) {
+    const uint64_t n_tiles = (totals[0] + L - 1) / L;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        totals[2] = n_tiles;
+        totals[3] = bigoff[totals[1]];
+        totals[5] = (totals[3] <= items_cap && totals[4] <= 4095) ? 1 : 0;
+    }
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= n_tiles;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        if (k == n_tiles) {
+            tile_first[k] = nb;
+            continue;
+        }
+        const uint64_t target = k * L;
+        uint64_t lo = 0, hi = nb;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (mpre[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        tile_first[k] = lo;
+    }
+}
+
+// ------------------------------------------------ generic path (t > 128)
+__device__ __forceinline__ uint32_t gmask16(const uint32_t* __restrict__ tags, uint64_t n,
+                                            uint32_t W, uint32_t a, uint32_t b, int w) {
     uint32_t x = 0xFFFFFFFFu;
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-        const uint4 u = __ldg(pa + qq), v = __ldg(pb + qq);
-        x &= ~(u.x ^ v.x) & ~(u.y ^ v.y) & ~(u.z ^ v.z) & ~(u.w ^ v.w);
+    for (int g = 0; g < 2; ++g) {
+        const uint4* pa = (const uint4*)(tags + ((uint64_t)g * n + a) * W * 8 + w * 8);
+        const uint4* pb = (const uint4*)(tags + ((uint64_t)g * n + b) * W * 8 + w * 8);
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+            const uint4 u = __ldg(pa + qq), v = __ldg(pb + qq);
+            x &= ~(u.x ^ v.x) & ~(u.y ^ v.y) & ~(u.z ^ v.z) & ~(u.w ^ v.w);
+        }
     }
     return x;
 }
@@ -371,7 +701,7 @@ __global__ void __launch_bounds__(256) k_pairs_generic(
     const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
     const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
     const uint64_t* __restrict__ chunk_off, uint64_t nb, const uint64_t* __restrict__ rkeys,
-    const uint32_t* __restrict__ tags, uint32_t t, uint32_t m, uint64_t excl,
+    const uint32_t* __restrict__ tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
     const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges, uint32_t p, int mode,
     uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
     unsigned long long* __restrict__ counters) {
@@ -403,7 +733,7 @@ __global__ void __launch_bounds__(256) k_pairs_generic(
             bool first = true;
             uint32_t exact = 0;
             for (uint32_t w = 0; w < W; ++w) {
-                uint32_t x = gmask16(tags, W, a, bid, (int)w);
+                uint32_t x = gmask16(tags, n, W, a, bid, (int)w);
                 if (w == W - 1 && (t & 31)) x &= (1u << (t & 31)) - 1u;
                 while (x) {
                     const uint32_t tt = w * 32 + __ffs(x) - 1;
@@ -437,38 +767,65 @@ __global__ void k_chunk_counts(const uint32_t* __restrict__ bsize, uint64_t nb,
         off[i] = i < nb ? (bsize[i] + 31) / 32 : 0;
 }
 
+// ------------------------------------------------------------------ launch
 template <int W, int MODE, bool HAS_E>
-static int launch_pairs(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
-                        const uint32_t* btab, const uint64_t* off, uint64_t nb,
-                        const uint64_t* rkeys, const uint32_t* tags, uint32_t t, uint32_t m,
-                        uint64_t excl, const uint8_t* emask, const uint64_t* edges, uint32_t p,
-                        uint64_t* out_key, uint32_t* out_sim, uint64_t cap,
-                        unsigned long long* counters, unsigned long long* work, cudaStream_t st) {
-    using C = PairCfg<W, MODE>;
-    const size_t smem = (size_t)C::WARPS * C::PER_WARP * 4;
-    auto kern = k_pairs<W, MODE, HAS_E>;
-    QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
+                  const uint32_t* btab, uint64_t nb, const uint64_t* rkeys, const uint32_t* tags,
+                  uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
+                  const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
+                  uint64_t cap, unsigned long long* counters, uint64_t* ws, void* sws,
+                  cudaStream_t st) {
+    using C = TileCfg<W, MODE>;
+    const uint32_t L = C::L;
+    uint64_t* mpre = ws;                       // nb + 1
+    uint64_t* bigpos = mpre + (nb + 1);        // nb + 1
+    uint64_t* bigb = bigpos + (nb + 1);        // nb + 1
+    uint64_t* bigoff = bigb + (nb + 1);        // nb + 1
+    uint64_t* tile_first = bigoff + (nb + 1);  // nb + 1
+    uint64_t* items = tile_first + (nb + 1);   // <= 8 (nb + 1)
+    uint64_t* totals = items + (nb + 1) * 8;   // 6
+    unsigned long long* work = (unsigned long long*)(totals + 6);
+    const uint64_t items_cap = (nb + 1) * 8;
+    const unsigned g = qs_blocks(nb + 1, 256);
+    k_plan_sizes<<<g, 256, 0, st>>>(bsize, nb, L, mpre, bigpos);
+    int rc = scan_u64(mpre, mpre, nb + 1, totals + 0, sws, st);
+    if (rc) return rc;
+    rc = scan_u64(bigpos, bigpos, nb + 1, totals + 1, sws, st);
+    if (rc) return rc;
+    QS_CUDA(cudaMemsetAsync(bigoff, 0, (nb + 1) * 8, st), "memset");
+    QS_CUDA(cudaMemsetAsync(totals + 4, 0, 8, st), "memset");
+    k_plan_big<<<g, 256, 0, st>>>(bsize, nb, L, bigpos, bigb, bigoff,
+                                  (unsigned long long*)(totals + 4));
+    rc = scan_u64(bigoff, bigoff, nb + 1, nullptr, sws, st);
+    if (rc) return rc;
+    k_plan_tiles<<<g, 256, 0, st>>>(mpre, nb, L, totals, bigoff, tile_first, items_cap);
+    k_plan_bigitems<<<g, 256, 0, st>>>(bsize, bigb, bigoff, totals, L, items, items_cap);
+    QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
+    QS_CHECK_LAUNCH("plan");
+    Plan plan{mpre, tile_first, items, bigb, bigoff, totals};
+    auto kern = k_pairs_pc<W, MODE, HAS_E>;
+    QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM),
             "smem attr");
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PTHREADS, C::SMEM);
     if (per_sm < 1) per_sm = 1;
-    kern<<<num_sms() * per_sm, C::WARPS * 32, smem, st>>>(sids, bstart, bsize, btab, off, nb, rkeys,
-                                                         tags, t, m, excl, emask, edges, p, out_key,
-                                                         out_sim, cap, counters, work);
-    QS_CHECK_LAUNCH("k_pairs");
+    kern<<<num_sms() * per_sm, PTHREADS, C::SMEM, st>>>(sids, bstart, bsize, btab, plan, rkeys, tags,
+                                                        n, t, m, excl, emask, edges, p, out_key,
+                                                        out_sim, cap, counters, work);
+    QS_CHECK_LAUNCH("k_pairs_pc");
     return QS_OK;
 }
 
 template <int W>
 static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint64_t* bstart,
-                         const uint32_t* bsize, const uint32_t* btab, const uint64_t* off,
-                         uint64_t nb, const uint64_t* rkeys, const uint32_t* tags, uint32_t t,
+                         const uint32_t* bsize, const uint32_t* btab, uint64_t nb,
+                         const uint64_t* rkeys, const uint32_t* tags, uint64_t n, uint32_t t,
                          uint32_t m, uint64_t excl, const uint8_t* emask, const uint64_t* edges,
                          uint32_t p, uint64_t* ok, uint32_t* os, uint64_t cap,
-                         unsigned long long* counters, unsigned long long* work, cudaStream_t st) {
+                         unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
 #define QS_L(MM, EE) \
-    launch_pairs<W, MM, EE>(sids, bstart, bsize, btab, off, nb, rkeys, tags, t, m, excl, emask, \
-                            edges, p, ok, os, cap, counters, work, st)
+    run_pc<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, p, \
+                      ok, os, cap, counters, ws, sws, st)
     if (mode == MODE_FULL) return has_e ? QS_L(MODE_FULL, true) : QS_L(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_L(MODE_MATCHED, true) : QS_L(MODE_MATCHED, false);
     return has_e ? QS_L(MODE_DISTINCT, true) : QS_L(MODE_DISTINCT, false);
@@ -481,8 +838,23 @@ using namespace qs;
 
 extern "C" {
 
+#ifdef QS_PROF
+int qs_prof_read(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, qs::g_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(qs::g_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+// big-bucket items: a bucket of s > L members gives nseg(nseg+1)/2 items with
+// nseg = ceil(s / L) < 2s / L, i.e. fewer than 2 s^2 / L^2 items <= 8 per
+// member-bucket slot for s <= 4L; larger buckets are bounded by the member
+// count (s / L items per segment row), so 8 slots per bucket bound the table.
 size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle) {
-    return (size_t)(n_nonsingle + 2) * 8 + scan_ws_bytes(n_nonsingle + 1) + 512;
+    return (size_t)(n_nonsingle + 1) * 8 * (5 + 8) + 64 + scan_ws_bytes(n_nonsingle + 1) + 512;
 }
 
 int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
@@ -491,38 +863,36 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
                  const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
                  uint64_t* out_key_dev, uint32_t* out_sim_dev, uint64_t cap,
                  unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes, void* stream) {
-    (void)n;
     cudaStream_t st = (cudaStream_t)stream;
     QS_ARG(ws_bytes >= qs_lsh_pairs_ws_bytes(n_nonsingle), "pairs workspace too small");
     QS_ARG(m >= 1 && m <= t, "min_matches must be in [1, tables]");
     QS_ARG(mode >= 0 && mode <= 2, "mode must be 0 (full), 1 (matched) or 2 (distinct)");
-    QS_ARG(t <= (1u << 24), "too many tables");
     if (n_nonsingle == 0) return QS_OK;
-    uint64_t* off = (uint64_t*)ws_dev;
-    unsigned long long* work = (unsigned long long*)(off + n_nonsingle + 1);
-    void* sws = (void*)(((uintptr_t)(work + 1) + 63) & ~(uintptr_t)63);
-    k_chunk_counts<<<qs_blocks(n_nonsingle + 1, 256), 256, 0, st>>>(bsize_dev, n_nonsingle, off);
-    int rc = scan_u64(off, off, n_nonsingle + 1, nullptr, sws, st);
-    if (rc) return rc;
-    QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
+    const uint64_t nb = n_nonsingle;
+    uint64_t* ws = (uint64_t*)ws_dev;
+    void* sws = (void*)(((uintptr_t)(ws + (nb + 1) * 13 + 8) + 63) & ~(uintptr_t)63);
     const uint32_t W = (t + 31) >> 5;
     const bool has_e = excluded_dev != nullptr;
 #define QS_D(WW)                                                                                  \
-    dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, off, n_nonsingle,   \
-                      rkeys_dev, tags_dev, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,   \
-                      out_sim_dev, cap, counters_dev, work, st)
+    dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, nb, rkeys_dev,      \
+                      tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,           \
+                      out_sim_dev, cap, counters_dev, ws, sws, st)
     switch (W) {
         case 1: return QS_D(1);
         case 2: return QS_D(2);
         case 3: return QS_D(3);
         case 4: return QS_D(4);
-        default:
+        default: {
+            uint64_t* off = ws;
+            k_chunk_counts<<<qs_blocks(nb + 1, 256), 256, 0, st>>>(bsize_dev, nb, off);
+            int rc = scan_u64(off, off, nb + 1, nullptr, sws, st);
+            if (rc) return rc;
             k_pairs_generic<<<num_sms() * 8, 256, 0, st>>>(
-                sids_dev, bstart_dev, bsize_dev, btab_dev, off, n_nonsingle, rkeys_dev, tags_dev, t,
-                m, excl, excluded_dev, edges_dev, p, mode, out_key_dev, out_sim_dev, cap,
-                counters_dev);
+                sids_dev, bstart_dev, bsize_dev, btab_dev, off, nb, rkeys_dev, tags_dev, n, t, m,
+                excl, excluded_dev, edges_dev, p, mode, out_key_dev, out_sim_dev, cap, counters_dev);
             QS_CHECK_LAUNCH("k_pairs_generic");
             return QS_OK;
+        }
     }
 #undef QS_D
 }

@@ -407,7 +407,7 @@ def search_signatures(sigs, cfg: SearchConfig, exclusion_windows: int = 0):
     W = (t + 31) // 32
     keys = torch.empty((t, n), dtype=torch.int64, device=sdev.device)
     rkeys = torch.empty((n, t), dtype=torch.int64, device=sdev.device)
-    tags = torch.empty((n, W, 16), dtype=torch.int32, device=sdev.device)
+    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=sdev.device)
     nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
              nat.stream())
     trip, stats, _ = run_search(keys, rkeys, tags, n, t, cfg, exclusion_windows)
@@ -426,7 +426,7 @@ def signatures_for_search(bits, mapping: HashMapping):
     _, plan = mapping.device_plan()
     keys = torch.empty((t, n), dtype=torch.int64, device=bits.device)
     rkeys = torch.empty((n, t), dtype=torch.int64, device=bits.device)
-    tags = torch.empty((n, W, 16), dtype=torch.int32, device=bits.device)
+    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=bits.device)
     bad = torch.zeros(1, dtype=torch.int32, device=bits.device)
     nat.call("qs_minmax_signatures_search", nat.ptr(bits), n, K, nat.ptr(plan), mapping.d, t,
              mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags), nat.ptr(bad),
