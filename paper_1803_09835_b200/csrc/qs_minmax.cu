@@ -28,12 +28,15 @@ __global__ void k_gen_mapping(uint64_t* __restrict__ v, uint32_t d, uint32_t F, 
 // ----------------------------------------------------------------- plan
 constexpr uint32_t PLAN_MAX_D = 16384;  // smem bitonic sort capacity (192 KB)
 
+// Plan layout, probe-sequence-major so one probe sequence walks consecutive
+// addresses (L1-resident prefixes): order[side][f][r], svals[side][f][r] with
+// side 0 = ascending value order (minimum probes), side 1 = descending (maximum).
 static inline size_t plan_order_bytes(uint32_t d, uint32_t F) {
-    return (((size_t)d * F * sizeof(uint16_t)) + 255) & ~(size_t)255;
+    return (((size_t)2 * d * F * sizeof(uint16_t)) + 255) & ~(size_t)255;
 }
 
 // One CTA per hash column: bitonic sort of (value, element) in shared memory,
-// then scatter into the rank-major plan (order[r * F + f], svals[r * F + f]).
+// then write both probe directions of the column into the plan.
 __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, uint32_t d,
                                                uint32_t F, uint32_t dpad,
                                                uint16_t* __restrict__ order,
@@ -71,8 +74,11 @@ __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, u
         }
     }
     for (uint32_t r = threadIdx.x; r < d; r += blockDim.x) {
-        order[(uint64_t)r * F + f] = (uint16_t)idx[r];
-        svals[(uint64_t)r * F + f] = key[r];
+        const uint64_t up = (uint64_t)f * d + r, down = ((uint64_t)F + f) * d + r;
+        order[up] = (uint16_t)idx[r];
+        svals[up] = key[r];
+        order[down] = (uint16_t)idx[d - 1 - r];
+        svals[down] = key[d - 1 - r];
     }
 }
 
@@ -80,7 +86,9 @@ __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, u
 __device__ __forceinline__ uint64_t mix_key(uint64_t s) { return fmix64(s ^ GOLDEN64); }
 
 // One warp per fingerprint row (grid-stride).  Shared memory per warp: the
-// d-bit bitmap and the 2F probe results.
+// d-bit bitmap and the rank at which each of the 2F probe sequences hit.  The
+// probe loop only touches the (L1-resident) prefixes of the order array; the
+// hit values are gathered afterwards with independent loads.
 template <bool SEARCH>
 __global__ void __launch_bounds__(256) k_signatures(
     const uint32_t* __restrict__ bits, uint64_t n, uint32_t K,
@@ -91,9 +99,9 @@ __global__ void __launch_bounds__(256) k_signatures(
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t words = (d + 31) >> 5;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t per_warp = ((words * 4 + 15) & ~15u) + 2 * F * 8;
+    const uint32_t per_warp = ((words * 4 + 15) & ~15u) + ((2 * F * 2 + 15) & ~15u);
     uint32_t* bm = (uint32_t*)(smem + warp * per_warp);
-    uint64_t* vals = (uint64_t*)((unsigned char*)bm + ((words * 4 + 15) & ~15u));
+    uint16_t* rk = (uint16_t*)((unsigned char*)bm + ((words * 4 + 15) & ~15u));
     const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t W = (t + 31) >> 5;
@@ -127,17 +135,14 @@ __global__ void __launch_bounds__(256) k_signatures(
         // merged probe loop: lane walks its columns seq = lane, lane+32, ... < 2F
         uint32_t seq = lane, r = 0;
         while (seq < 2 * F) {
-            const bool is_min = seq < F;
-            const uint32_t f = is_min ? seq : seq - F;
-            const uint32_t rank = is_min ? r : d - 1 - r;
-            const uint64_t pos = (uint64_t)rank * F + f;
+            const uint64_t pos = (uint64_t)seq * d + r;  // seq < F: minimum side, else maximum
             const uint32_t x = __ldg(order + pos);
             if ((bm[x >> 5] >> (x & 31)) & 1u) {
-                vals[seq] = __ldg(svals + pos);
+                rk[seq] = (uint16_t)r;
                 seq += 32;
                 r = 0;
             } else if (++r >= d) {  // only reachable when every bit was invalid
-                vals[seq] = 0;
+                rk[seq] = 0;
                 seq += 32;
                 r = 0;
             }
@@ -147,10 +152,14 @@ __global__ void __launch_bounds__(256) k_signatures(
             const uint32_t i = wr * 32 + lane;
             uint64_t acc = 0;
             if (i < t) {
-                const uint64_t* mn = vals + (uint64_t)i * kh;
-                const uint64_t* mx = vals + F + (uint64_t)i * kh;
-                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mn[j]);
-                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mx[j]);
+                for (uint32_t j = 0; j < kh; ++j) {
+                    const uint32_t sq = i * kh + j;
+                    acc = combine1(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
+                }
+                for (uint32_t j = 0; j < kh; ++j) {
+                    const uint32_t sq = F + i * kh + j;
+                    acc = combine1(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
+                }
                 if (sigs) sigs[row * t + i] = acc;
             }
             if (SEARCH) {
@@ -175,7 +184,7 @@ __global__ void __launch_bounds__(256) k_signatures(
 
 static size_t sig_smem_per_warp(uint32_t d, uint32_t F) {
     uint32_t words = (d + 31) >> 5;
-    return ((words * 4 + 15) & ~15u) + 2 * (size_t)F * 8;
+    return ((words * 4 + 15) & ~15u) + (((size_t)2 * F * 2 + 15) & ~(size_t)15);
 }
 
 static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
@@ -235,7 +244,7 @@ int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs, uint
 }
 
 size_t qs_minmax_plan_bytes(uint32_t d, uint32_t n_funcs) {
-    return plan_order_bytes(d, n_funcs) + (size_t)d * n_funcs * sizeof(uint64_t);
+    return plan_order_bytes(d, n_funcs) + (size_t)2 * d * n_funcs * sizeof(uint64_t);
 }
 
 int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs, void* plan_dev,
