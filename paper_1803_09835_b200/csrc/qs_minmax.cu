@@ -133,18 +133,43 @@ __global__ void __launch_bounds__(256) k_signatures(
         if (__any_sync(0xffffffffu, badrow) && lane == 0) atomicExch(bad, 1u);
         __syncwarp();
         // merged probe loop: lane walks its columns seq = lane, lane+32, ... < 2F
+        // (seq < F: minimum side, else maximum), eight ranks per step when the
+        // plan rows are 16-byte aligned (d % 8 == 0)
         uint32_t seq = lane, r = 0;
-        while (seq < 2 * F) {
-            const uint64_t pos = (uint64_t)seq * d + r;  // seq < F: minimum side, else maximum
-            const uint32_t x = __ldg(order + pos);
-            if ((bm[x >> 5] >> (x & 31)) & 1u) {
-                rk[seq] = (uint16_t)r;
-                seq += 32;
-                r = 0;
-            } else if (++r >= d) {  // only reachable when every bit was invalid
-                rk[seq] = 0;
-                seq += 32;
-                r = 0;
+        const uint16_t* ord = order + (uint64_t)seq * d;
+        if ((d & 7) == 0) {
+            while (seq < 2 * F) {
+                const uint4 v = __ldg((const uint4*)(ord + r));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                uint32_t h = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t xa = w[e] & 0xFFFFu, xb = w[e] >> 16;
+                    h |= ((bm[xa >> 5] >> (xa & 31)) & 1u) << (2 * e);
+                    h |= ((bm[xb >> 5] >> (xb & 31)) & 1u) << (2 * e + 1);
+                }
+                r += 8;
+                if (h || r >= d) {  // r >= d only when every bit was invalid
+                    rk[seq] = h ? (uint16_t)(r - 8 + __ffs(h) - 1) : (uint16_t)0;
+                    seq += 32;
+                    r = 0;
+                    ord += (uint64_t)32 * d;
+                }
+            }
+        } else {
+            while (seq < 2 * F) {
+                const uint32_t x = __ldg(ord + r);
+                if ((bm[x >> 5] >> (x & 31)) & 1u) {
+                    rk[seq] = (uint16_t)r;
+                    seq += 32;
+                    r = 0;
+                    ord += (uint64_t)32 * d;
+                } else if (++r >= d) {
+                    rk[seq] = 0;
+                    seq += 32;
+                    r = 0;
+                    ord += (uint64_t)32 * d;
+                }
             }
         }
         __syncwarp();
