@@ -166,6 +166,44 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
     }
 }
 
+// After a sort on the top 32 key bits: each run of equal prefix is scanned by
+// the thread at its start; if its full keys are not already grouped, the run
+// is insertion-sorted by full key (stable, so ids stay ascending per key).
+// Runs are short (mixed runs are rare prefix collisions), so cost ~ one pass.
+__global__ void k_fix_prefix_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                  uint64_t n, uint64_t total) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pos = g % n;
+        const uint64_t k0 = keys[g];
+        if (pos != 0 && (keys[g - 1] >> 32) == (k0 >> 32)) continue;  // not a run start
+        const uint64_t seg_end = g - pos + n;
+        uint64_t e = g + 1;
+        bool sorted = true;
+        uint64_t prev = k0;
+        while (e < seg_end) {
+            const uint64_t k = keys[e];
+            if ((k >> 32) != (k0 >> 32)) break;
+            if (k < prev) sorted = false;
+            prev = k;
+            ++e;
+        }
+        if (sorted) continue;
+        for (uint64_t i = g + 1; i < e; ++i) {
+            const uint64_t key = keys[i];
+            const uint32_t id = ids[i];
+            uint64_t j = i;
+            while (j > g && keys[j - 1] > key) {
+                keys[j] = keys[j - 1];
+                ids[j] = ids[j - 1];
+                --j;
+            }
+            keys[j] = key;
+            ids[j] = id;
+        }
+    }
+}
+
 __global__ void k_iota_segments(uint32_t* __restrict__ ids, uint64_t n, uint32_t t) {
     uint64_t total = n * t;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -506,13 +544,18 @@ int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t, uint6
     k_iota_segments<<<qs_blocks(total, 256), 256, 0, st>>>(ids_out_dev, n, t);
     QS_CHECK_LAUNCH("k_iota_segments");
     int in_alt = 0;
+    // keys are fmix64-mixed, so their top 32 bits already separate almost every
+    // pair of distinct keys: sort on bits [32, 64) only (4 passes instead of 8),
+    // then restore full-key order inside the rare runs whose prefixes collide.
     int rc = radix_sort_pairs(keys_out_dev, ids_out_dev, n, t, 64, alt_k, alt_v, rws,
-                              radix_ws_bytes(n, t), &in_alt, st);
+                              radix_ws_bytes(n, t), &in_alt, st, 32);
     if (rc) return rc;
     if (in_alt) {
         QS_CUDA(cudaMemcpyAsync(keys_out_dev, alt_k, total * 8, cudaMemcpyDeviceToDevice, st), "copy");
         QS_CUDA(cudaMemcpyAsync(ids_out_dev, alt_v, total * 4, cudaMemcpyDeviceToDevice, st), "copy");
     }
+    k_fix_prefix_runs<<<qs_blocks(total, 256), 256, 0, st>>>(keys_out_dev, ids_out_dev, n, total);
+    QS_CHECK_LAUNCH("k_fix_prefix_runs");
     return QS_OK;
 }
 

@@ -80,20 +80,29 @@ __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* __restrict__ hist, u
     }
 }
 
+// Stable scatter of one tile: rank in input order per digit, stage the tile in
+// shared memory in (digit, input) order, then write each digit's run to its
+// global slot with consecutive threads on consecutive addresses (coalesced).
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
     const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t seg_len,
     uint32_t tiles, uint32_t shift, const uint32_t* __restrict__ offs,
     uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals) {
+    extern __shared__ __align__(16) unsigned char rs_smem[];
+    uint64_t* sk = (uint64_t*)rs_smem;                  // [RS_TILE]
+    uint32_t* sv = (uint32_t*)(sk + RS_TILE);           // [RS_TILE]
     __shared__ uint32_t wcnt[RS_WARPS][RS_RADIX];
-    __shared__ uint32_t toff[RS_RADIX];
+    __shared__ uint32_t dstart[RS_RADIX];   // digit run start inside the tile
+    __shared__ uint32_t goff[RS_RADIX];     // digit run start in the output segment
     const uint32_t tile = blockIdx.x, seg = blockIdx.y;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < RS_WARPS * RS_RADIX; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
     for (int dgt = threadIdx.x; dgt < RS_RADIX; dgt += RS_THREADS)
-        toff[dgt] = offs[((uint64_t)seg * RS_RADIX + dgt) * tiles + tile];
+        goff[dgt] = offs[((uint64_t)seg * RS_RADIX + dgt) * tiles + tile];
     __syncthreads();
     const uint64_t base = (uint64_t)seg * seg_len;
-    const uint64_t t0 = (uint64_t)tile * RS_TILE + (uint64_t)warp * (32 * RS_ITEMS);
+    const uint64_t tile0 = (uint64_t)tile * RS_TILE;
+    const uint32_t tile_n = (uint32_t)min((uint64_t)RS_TILE, seg_len - tile0);
+    const uint64_t t0 = tile0 + (uint64_t)warp * (32 * RS_ITEMS);
     uint64_t k[RS_ITEMS];
     uint32_t v[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
@@ -116,14 +125,38 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         __syncwarp();
     }
     __syncthreads();
-    // exclusive prefix across warps per digit
-    for (int dgt = threadIdx.x; dgt < RS_RADIX; dgt += RS_THREADS) {
-        uint32_t run = toff[dgt];
+    // per digit: tile-local run start and per-warp offsets inside the run
+    if (threadIdx.x < RS_RADIX) {
+        const uint32_t dgt = threadIdx.x;
+        uint32_t run = 0;
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) {
-            uint32_t c = wcnt[w][dgt];
+            const uint32_t c = wcnt[w][dgt];
             wcnt[w][dgt] = run;
             run += c;
+        }
+        dstart[dgt] = run;  // digit total for now
+    }
+    __syncthreads();
+    // exclusive scan of digit totals (256 entries) by warp 0
+    if (warp == 0) {
+        uint32_t tot[8], s = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            tot[e] = dstart[lane * 8 + e];
+            s += tot[e];
+        }
+        uint32_t x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        uint32_t ex = x - s;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            dstart[lane * 8 + e] = ex;
+            ex += tot[e];
         }
     }
     __syncthreads();
@@ -132,10 +165,18 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         const uint64_t i = t0 + (uint64_t)r * 32 + lane;
         if (i < seg_len) {
             const uint32_t dgt = (uint32_t)((k[r] >> shift) & 0xFF);
-            const uint64_t pos = base + wcnt[warp][dgt] + rank[r];
-            okeys[pos] = k[r];
-            ovals[pos] = v[r];
+            const uint32_t lp = dstart[dgt] + wcnt[warp][dgt] + rank[r];
+            sk[lp] = k[r];
+            sv[lp] = v[r];
         }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tile_n; j += RS_THREADS) {
+        const uint64_t key = sk[j];
+        const uint32_t dgt = (uint32_t)((key >> shift) & 0xFF);
+        const uint64_t pos = base + goff[dgt] + (j - dstart[dgt]);
+        okeys[pos] = key;
+        ovals[pos] = sv[j];
     }
 }
 
@@ -147,7 +188,7 @@ size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments) {
 
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
                      uint32_t key_bits, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
-                     size_t ws_bytes, int* in_alt, cudaStream_t st) {
+                     size_t ws_bytes, int* in_alt, cudaStream_t st, uint32_t bit_lo) {
     *in_alt = 0;
     if (seg_len == 0 || segments == 0 || key_bits == 0) return QS_OK;
     QS_ARG(seg_len < (1ull << 32), "radix sort segment longer than 2^32");
@@ -155,14 +196,16 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t 
     const uint32_t tiles = rs_tiles(seg_len);
     QS_ARG(tiles <= 65535u * 64u, "too many tiles");
     uint32_t* hist = (uint32_t*)ws;
+    QS_CUDA(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 RS_TILE * 12), "smem attr");
     uint64_t *src_k = keys, *dst_k = keys_alt;
     uint32_t *src_v = vals, *dst_v = vals_alt;
-    for (uint32_t shift = 0; shift < key_bits; shift += 8) {
+    for (uint32_t shift = bit_lo; shift < key_bits; shift += 8) {
         dim3 grid(tiles, segments);
         k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
         k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
-        k_rs_scatter<<<grid, RS_THREADS, 0, st>>>(src_k, src_v, seg_len, tiles, shift, hist,
-                                                  dst_k, dst_v);
+        k_rs_scatter<<<grid, RS_THREADS, RS_TILE * 12, st>>>(src_k, src_v, seg_len, tiles, shift,
+                                                             hist, dst_k, dst_v);
         QS_CHECK_LAUNCH("radix sort pass");
         uint64_t* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
@@ -186,7 +229,7 @@ int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len
     QS_ARG(key_bits <= 64, "key_bits must be <= 64");
     return qs::radix_sort_pairs(keys_dev, vals_dev, seg_len, segments, key_bits, keys_alt_dev,
                                 vals_alt_dev, ws_dev, ws_bytes, result_in_alt,
-                                (cudaStream_t)stream);
+                                (cudaStream_t)stream, 0);
 }
 
 }  // extern "C"
