@@ -183,6 +183,57 @@ int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_p
                     uint32_t key_bits, uint8_t* triplets_dev, void* ws_dev, size_t ws_bytes,
                     void* stream);
 
+/* ------------------------------------------------------------ fingerprinting
+ * Chain of fingerprint.fingerprint_series (fingerprint.py:581-623).  Float64
+ * compute with float32 storage at the reference's rounding points
+ * (spectrogram :148-149, images :239-241, coefficients :334). */
+
+/* Band-limited log-power STFT (fingerprint.py:136-151 restricted to the band
+ * rows): out[c, b] = float32(log10(|sum_j x[c*hop + j] tw[b, j]|^2 + 1e-12))
+ * for c < n_cols, where tw (nb, frame, 2) float64 = hanning taper times the
+ * DFT twiddles of the band bins.  Samples are float64 (x_is_f32 = 0) or
+ * float32 widened exactly (x_is_f32 = 1). */
+int qs_fp_band_stft(const void* x_dev, int x_is_f32, uint64_t n_samples, uint32_t frame,
+                    uint32_t hop, uint64_t n_cols, uint32_t nb, const double* tw_dev,
+                    float* out_dev, void* stream);
+
+/* Per fingerprint window (iter_image_batches / iter_coeff_batches /
+ * topk_bits, fingerprint.py:198-243, 271-335, 433-466): band rows ->
+ * area-resampled image (CSR weights w_f over band rows, w_t per window width
+ * in [wmin, wmax]) -> 2-D Haar (sched: n_levels (h, w, mode) triples, mode
+ * bit 0 = row pass, bit 1 = column pass) -> coefficients.  Windows are
+ * widx_dev[0..n_win) or win0 + [0, n_win).  mode 0: images (n_win, F, T) f32;
+ * 1: coefficients (n_win, F*T) f32; 2: coefficients column-major (F*T, n_win);
+ * 3: top_k sign bits (n_win, top_k) u32 using med/mad.  A non-finite
+ * coefficient sets bit 0 of *flags_dev (-> DataError). */
+int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int64_t* widx_dev,
+                  uint64_t win0, uint64_t n_win, uint64_t lag, uint64_t win, uint32_t frame,
+                  uint32_t hop, const int32_t* wf_off, const int32_t* wf_idx, const double* wf_val,
+                  const int32_t* wt_off, const int32_t* wt_idx, const double* wt_val,
+                  uint32_t wmin, uint32_t wmax, uint32_t F, uint32_t T, const int32_t* sched_dev,
+                  uint32_t n_levels, int mode, const double* med_dev, const double* mad_dev,
+                  uint32_t top_k, void* out_dev, uint32_t* flags_dev, void* stream);
+
+/* Median and MAD of each of n_coeffs columns of S float32 values (column-major
+ * (n_coeffs, S)), float64 results exactly as np.median / np.median(|x - med|)
+ * (estimate_mad, fingerprint.py:376-384).  ws_dev: 2 * n_coeffs doubles. */
+int qs_fp_mad(const float* cols_dev, uint32_t n_coeffs, uint64_t S, double* med_dev,
+              double* mad_dev, double* ws_dev, void* stream);
+
+/* topk_bits (fingerprint.py:433-466) of B rows of n coefficients (float32, or
+ * float64 with is_f64). */
+int qs_fp_topk_bits(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
+                    const double* med_dev, const double* mad_dev, uint32_t top_k, uint32_t* out_dev,
+                    uint32_t* flags_dev, void* stream);
+
+/* haar2d / ihaar2d (fingerprint.py:271-323) of B float64 (H, W) images in place. */
+int qs_fp_haar2d(double* data_dev, uint64_t B, uint32_t H, uint32_t W, const int32_t* sched_dev,
+                 uint32_t n_levels, int inverse, void* stream);
+
+/* normalize (fingerprint.py:425-430): (c - median)/MAD, 0 where MAD == 0. */
+int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const double* med_dev,
+                    const double* mad_dev, double* out_dev, void* stream);
+
 /* Generic stable LSD radix sort of (uint64 key, uint32 value) pairs over
  * `segments` independent equal-length segments, on key bits [0, key_bits). */
 size_t qs_radix_sort_ws_bytes(uint64_t seg_len, uint32_t segments);

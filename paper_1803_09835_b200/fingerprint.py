@@ -151,3 +151,354 @@ def jaccard(bits_a, bits_b) -> float:
         return 1.0
     inter = np.intersect1d(a, b, assume_unique=True).size
     return inter / (a.size + b.size - inter)
+
+
+# ---------------------------------------------------------------------------
+# device chain (csrc/qs_fingerprint.cu)
+
+from functools import lru_cache  # noqa: E402
+
+from . import _native as nat  # noqa: E402
+from .errors import ConsistencyError, DataError  # noqa: E402
+
+_LOG_EPS = 1e-12
+
+
+def _stft_geometry(ts, params: FingerprintParams):
+    sr = ts.sample_rate_hz
+    frame = int(round(params.stft.frame_len_s * sr))
+    hop = max(1, int(round(params.stft.hop_s * sr)))
+    if frame < 2:
+        raise ParameterError("STFT frame shorter than 2 samples")
+    if ts.n_samples < frame:
+        raise DataError("series shorter than one STFT frame")
+    return frame, hop
+
+
+def _band_rows(freqs: np.ndarray, params: FingerprintParams):
+    """Rows inside the band corners (fingerprint.py:166-173)."""
+    if params.band_low_hz is None:
+        return 0, len(freqs)
+    keep = np.flatnonzero((freqs >= params.band_low_hz - 1e-9) & (freqs <= params.band_high_hz + 1e-9))
+    if keep.size == 0:
+        raise ParameterError("no spectrogram rows inside configured band")
+    return int(keep[0]), int(keep[-1]) + 1
+
+
+@lru_cache(maxsize=64)
+def _resize_weights(src: int, dst: int) -> np.ndarray:
+    """Area-overlap resampling matrix (dst, src); every row sums to 1 (fingerprint.py:176-186)."""
+    r = src / dst
+    w = np.zeros((dst, src))
+    for i in range(dst):
+        lo, hi = i * r, (i + 1) * r
+        for j in range(int(math.floor(lo)), min(int(math.ceil(hi)), src)):
+            w[i, j] = (min(hi, j + 1) - max(lo, j)) / r
+    w.setflags(write=False)
+    return w
+
+
+def _haar_schedule(h: int, w: int):
+    steps = []
+    while h % 2 == 0 and h > 1 and w % 2 == 0 and w > 1:
+        steps.append((h, w, 3))
+        h //= 2
+        w //= 2
+    while w % 2 == 0 and w > 1:
+        steps.append((h, w, 1))
+        w //= 2
+    while h % 2 == 0 and h > 1:
+        steps.append((h, w, 2))
+        h //= 2
+    return steps
+
+
+def _csr(mat: np.ndarray):
+    rows, cols = np.nonzero(mat)
+    off = np.zeros(mat.shape[0] + 1, np.int32)
+    np.add.at(off, rows + 1, 1)
+    return np.cumsum(off).astype(np.int32), cols.astype(np.int32), mat[rows, cols].astype(np.float64)
+
+
+class _Chain:
+    """Device state of one channel: samples, band spectrogram and the
+    window-kernel tables (geometry of fingerprint.py:198-243)."""
+
+    def __init__(self, ts, params: FingerprintParams, full_band: bool = False):
+        params.validate()
+        self.torch = torch = nat.torch()
+        self.params = params
+        sr = ts.sample_rate_hz
+        self.frame, self.hop = _stft_geometry(ts, params)
+        self.win = int(round(params.window_len_s * sr))
+        self.lag = max(1, int(round(params.window_lag_s * sr)))
+        self.n_win = n_windows(ts, params)
+        self.n_cols = (ts.n_samples - self.frame) // self.hop + 1
+        self.freqs = np.fft.rfftfreq(self.frame, 1.0 / sr)
+        self.r0, self.r1 = (0, len(self.freqs)) if full_band else _band_rows(self.freqs, params)
+        self.nb = self.r1 - self.r0
+        x = ts.samples
+        if nat.is_device_tensor(x):
+            xd = x.contiguous()
+            if xd.dtype not in (torch.float32, torch.float64):
+                xd = xd.to(torch.float64)
+        else:
+            xh = np.ascontiguousarray(x, dtype=np.float64)
+            # float32-representable traces travel as float32 (exact widening on the device)
+            x32 = xh.astype(np.float32)
+            xd = torch.from_numpy(x32 if np.array_equal(x32.astype(np.float64), xh) else xh).cuda()
+        self.x = xd
+        taper = np.hanning(self.frame)
+        j = np.arange(self.frame)
+        k = np.arange(self.r0, self.r1)[:, None]
+        ang = 2.0 * np.pi * ((k * j) % self.frame) / self.frame
+        tw = np.stack([taper * np.cos(ang), -taper * np.sin(ang)], axis=-1)
+        self.tw = torch.from_numpy(np.ascontiguousarray(tw)).cuda()
+        self.band = torch.empty((max(self.n_cols, 1), self.nb), dtype=torch.float32, device="cuda")
+        nat.call("qs_fp_band_stft", nat.ptr(self.x), int(self.x.dtype == torch.float32),
+                 ts.n_samples, self.frame, self.hop, self.n_cols, self.nb, nat.ptr(self.tw),
+                 nat.ptr(self.band), nat.stream())
+
+    def prepare_windows(self):
+        params, torch = self.params, self.torch
+        if self.n_win == 0:
+            raise DataError("series shorter than one fingerprint window")
+        if self.win < self.frame:
+            raise ParameterError("fingerprint window shorter than one STFT frame")
+        probe = np.arange(min(self.n_win, self.hop * 2 + 1), dtype=np.int64) * self.lag
+        c0 = -(-probe // self.hop)
+        c1 = (probe + self.win - self.frame) // self.hop + 1
+        widths = c1 - c0
+        if widths.min() < 1:
+            raise ParameterError("window contains no complete STFT frame")
+        self.wmin, self.wmax = int(widths.min()), int(widths.max())
+        F, T = params.freq_bins, params.time_bins
+        wf_off, wf_idx, wf_val = _csr(_resize_weights(self.nb, F))
+        offs, idxs, vals, base = [], [], [], 0
+        for width in range(self.wmin, self.wmax + 1):
+            o, i, v = _csr(_resize_weights(width, T))
+            offs.append(o + base)
+            idxs.append(i)
+            vals.append(v)
+            base += len(i)
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        self.wf = (dev(wf_off), dev(wf_idx), dev(wf_val))
+        self.wt = (dev(np.concatenate(offs)), dev(np.concatenate(idxs)), dev(np.concatenate(vals)))
+        sched = _haar_schedule(F, T)
+        self.n_levels = len(sched)
+        self.sched = dev(np.array(sched, np.int32).reshape(-1) if sched else np.zeros(3, np.int32))
+        self.flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def windows(self, mode, out, widx=None, win0=0, n=None, med=None, mad=None, top_k=0):
+        n = self.n_win if n is None else n
+        F, T = self.params.freq_bins, self.params.time_bins
+        nat.call("qs_fp_windows", nat.ptr(self.band), self.n_cols, self.nb, nat.ptr(widx), win0, n,
+                 self.lag, self.win, self.frame, self.hop, nat.ptr(self.wf[0]), nat.ptr(self.wf[1]),
+                 nat.ptr(self.wf[2]), nat.ptr(self.wt[0]), nat.ptr(self.wt[1]), nat.ptr(self.wt[2]),
+                 self.wmin, self.wmax, F, T, nat.ptr(self.sched), self.n_levels, mode, nat.ptr(med),
+                 nat.ptr(mad), top_k, nat.ptr(out), nat.ptr(self.flags), nat.stream())
+
+    def check_finite(self):
+        if int(self.flags.item()) & 1:
+            raise DataError("non-finite Haar coefficient")
+
+
+def spectrogram(ts, params: FingerprintParams | None = None):
+    """Full-series log-power spectrogram (fingerprint.py:154-163).
+
+    Returns (freqs_hz, column_epochs_s, logpow) with logpow (n_freqs, n_cols) float32."""
+    params = params or FingerprintParams()
+    ch = _Chain(ts, params, full_band=True)
+    times = ts.start_epoch_s + np.arange(ch.n_cols) * (ch.hop / ts.sample_rate_hz)
+    return ch.freqs, times, ch.band[: ch.n_cols].t().contiguous().cpu().numpy()
+
+
+def _window_indices(chain, indices):
+    if indices is None:
+        return np.arange(chain.n_win, dtype=np.int64)
+    idx = np.asarray(indices, dtype=np.int64)
+    if idx.size and (idx.min() < 0 or idx.max() >= chain.n_win):
+        raise ParameterError("window index out of range")
+    return idx
+
+
+def _iter_batches(ts, params, indices, batch, mode):
+    params.validate()
+    ch = _Chain(ts, params)
+    ch.prepare_windows()
+    idx = _window_indices(ch, indices)
+    torch = ch.torch
+    F, T = params.freq_bins, params.time_bins
+    for b0 in range(0, idx.size, batch):
+        sel = idx[b0: b0 + batch]
+        widx = torch.from_numpy(sel).cuda()
+        shape = (sel.size, F, T) if mode == 0 else (sel.size, F * T)
+        out = torch.empty(shape, dtype=torch.float32, device="cuda")
+        ch.windows(mode, out, widx=widx, n=sel.size)
+        epochs = ts.start_epoch_s + sel * params.window_lag_s
+        yield sel, epochs, out.cpu().numpy()
+
+
+def iter_image_batches(ts, params: FingerprintParams, indices=None, batch: int = 512):
+    """Yield (window_indices, start_epochs, images (B, F, T) float32) (fingerprint.py:198-243)."""
+    yield from _iter_batches(ts, params, indices, batch, 0)
+
+
+def iter_coeff_batches(ts, params: FingerprintParams, indices=None, batch: int = 512):
+    """Yield (window_indices, epochs, coeffs (B, F*T) float32) (fingerprint.py:326-335)."""
+    yield from _iter_batches(ts, params, indices, batch, 1)
+
+
+def compute_spectral_images(ts, params: FingerprintParams):
+    """Generator of SpectralImage over all windows of a channel (fingerprint.py:246-250)."""
+    for idx, epochs, images in iter_image_batches(ts, params):
+        for i, e, v in zip(idx, epochs, images):
+            yield SpectralImage(int(i), float(e), v)
+
+
+def _haar_call(a, inverse):
+    torch = nat.torch()
+    arr = np.array(a, dtype=np.float64, copy=True)
+    if arr.ndim < 2:
+        raise ParameterError("haar2d needs at least a 2-D array" if not inverse
+                             else "ihaar2d needs at least a 2-D array")
+    H, W = arr.shape[-2:]
+    sched = _haar_schedule(H, W)
+    if not sched or arr.size == 0:
+        return arr
+    dev = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+    sd = torch.from_numpy(np.array(sched, np.int32).reshape(-1)).cuda()
+    nat.call("qs_fp_haar2d", nat.ptr(dev), arr.size // (H * W), H, W, nat.ptr(sd), len(sched),
+             int(inverse), nat.stream())
+    return dev.cpu().numpy().reshape(arr.shape)
+
+
+def haar2d(a) -> np.ndarray:
+    """Full orthonormal 2-D Haar decomposition of (..., H, W) arrays (fingerprint.py:271-300)."""
+    return _haar_call(a, False)
+
+
+def ihaar2d(a) -> np.ndarray:
+    """Inverse of haar2d (fingerprint.py:303-323)."""
+    return _haar_call(a, True)
+
+
+def _mad_from_chain(ch, params, rate, seed, total):
+    torch = ch.torch
+    n_sample = max(1, int(round(rate * total)))
+    if n_sample >= total:
+        sample = np.arange(total)
+        n_sample = total
+    else:
+        rng = np.random.default_rng(seed)
+        sample = np.sort(rng.choice(total, size=n_sample, replace=False))
+    n_coeffs = params.n_coeffs
+    cols = torch.empty((n_coeffs, n_sample), dtype=torch.float32, device="cuda")
+    ch.windows(2, cols, widx=torch.from_numpy(sample.astype(np.int64)).cuda(), n=n_sample)
+    med = torch.empty(n_coeffs, dtype=torch.float64, device="cuda")
+    mad = torch.empty(n_coeffs, dtype=torch.float64, device="cuda")
+    ws = torch.empty(2 * n_coeffs, dtype=torch.float64, device="cuda")
+    nat.call("qs_fp_mad", nat.ptr(cols), n_coeffs, n_sample, nat.ptr(med), nat.ptr(mad), nat.ptr(ws),
+             nat.stream())
+    return med, mad, n_sample
+
+
+def estimate_mad(ts, params: FingerprintParams, rate: float = 0.1, seed: int = 0,
+                 batch: int = 512) -> MadStats:
+    """Median and MAD per Haar coefficient from a random sample of windows
+    (fingerprint.py:341-389); the sample is drawn by the reference's own numpy
+    RNG call, the coefficients and order statistics are computed on the GPU."""
+    params.validate()
+    if not 0 < rate <= 1:
+        raise ParameterError(f"sampling rate must be in (0, 1], got {rate}")
+    total = n_windows(ts, params)
+    if total == 0:
+        raise DataError("series shorter than one fingerprint window")
+    ch = _Chain(ts, params)
+    ch.prepare_windows()
+    med, mad, n_sample = _mad_from_chain(ch, params, rate, seed, total)
+    return MadStats(median=med.cpu().numpy(), mad=mad.cpu().numpy(), rate=float(rate),
+                    seed=int(seed), n_sampled=int(n_sample), n_total=int(total))
+
+
+def normalize(coeffs, stats: MadStats) -> np.ndarray:
+    """Deviation scores v' = (v - median) / MAD; zero-MAD columns give 0 (fingerprint.py:425-430)."""
+    torch = nat.torch()
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float32))
+    shape = c.shape
+    n = shape[-1]
+    cd = torch.from_numpy(c.reshape(-1, n)).cuda()
+    med = torch.from_numpy(np.ascontiguousarray(stats.median, np.float64)).cuda()
+    mad = torch.from_numpy(np.ascontiguousarray(stats.mad, np.float64)).cuda()
+    out = torch.empty(cd.shape, dtype=torch.float64, device="cuda")
+    nat.call("qs_fp_normalize", nat.ptr(cd), cd.shape[0], n, nat.ptr(med), nat.ptr(mad),
+             nat.ptr(out), nat.stream())
+    return out.cpu().numpy().reshape(shape)
+
+
+def topk_bits(coeffs, stats: MadStats, top_k: int) -> np.ndarray:
+    """Sign-encoded bit indices of the top_k most anomalous coefficients
+    (fingerprint.py:433-466): (B, top_k) uint32, ascending per row."""
+    torch = nat.torch()
+    c = np.atleast_2d(np.asarray(coeffs, dtype=np.float64))
+    n = c.shape[1]
+    if n != stats.n_coeffs:
+        raise ParameterError("coefficient count does not match MAD stats")
+    n_eligible = int(stats.eligible.sum())
+    if not 1 <= top_k <= n:
+        raise ParameterError(f"top_k must be in [1, {n}]")
+    if top_k > n_eligible:
+        raise ParameterError(f"top_k={top_k} exceeds {n_eligible} coefficients with nonzero MAD")
+    if not np.isfinite(c).all():
+        raise DataError("non-finite Haar coefficient")
+    cd = torch.from_numpy(np.ascontiguousarray(c)).cuda()
+    med = torch.from_numpy(np.ascontiguousarray(stats.median, np.float64)).cuda()
+    mad = torch.from_numpy(np.ascontiguousarray(stats.mad, np.float64)).cuda()
+    out = torch.empty((c.shape[0], top_k), dtype=torch.int32, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.call("qs_fp_topk_bits", nat.ptr(cd), 1, c.shape[0], n, nat.ptr(med), nat.ptr(mad), top_k,
+             nat.ptr(out), nat.ptr(flags), nat.stream())
+    return out.cpu().numpy().view(np.uint32)
+
+
+def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = None,
+                       mad_rate: float = 0.1, mad_seed: int = 0,
+                       batch: int = 512) -> tuple[FingerprintSet, MadStats]:
+    """Fingerprint every window of a channel (fingerprint.py:581-623).
+
+    One STFT of the series serves both the MAD sample and the main pass.
+    Host traces give host FingerprintSet.bits; a CUDA trace gives CUDA bits."""
+    params.validate()
+    torch = nat.torch()
+    total = n_windows(ts, params)
+    ch = _Chain(ts, params)
+    if total == 0:
+        raise DataError("series shorter than one fingerprint window")
+    ch.prepare_windows()
+    if stats is None:
+        if not 0 < mad_rate <= 1:
+            raise ParameterError(f"sampling rate must be in (0, 1], got {mad_rate}")
+        med, mad, n_sample = _mad_from_chain(ch, params, mad_rate, mad_seed, total)
+        stats = MadStats(median=med.cpu().numpy(), mad=mad.cpu().numpy(), rate=float(mad_rate),
+                         seed=int(mad_seed), n_sampled=int(n_sample), n_total=int(total))
+    else:
+        med = torch.from_numpy(np.ascontiguousarray(stats.median, np.float64)).cuda()
+        mad = torch.from_numpy(np.ascontiguousarray(stats.mad, np.float64)).cuda()
+    if stats.n_coeffs != params.n_coeffs:
+        raise ConsistencyError("MAD stats shape does not match params")
+    n_eligible = int(stats.eligible.sum())
+    if params.top_k > n_eligible:
+        raise ParameterError(f"top_k={params.top_k} exceeds {n_eligible} coefficients with nonzero MAD")
+    bits = torch.empty((total, params.top_k), dtype=torch.int32, device="cuda")
+    ch.windows(3, bits, win0=0, n=total, med=med, mad=mad, top_k=params.top_k)
+    ch.check_finite()
+    indices = np.arange(total, dtype=np.uint64)
+    epochs = ts.start_epoch_s + np.arange(total) * params.window_lag_s
+    out_bits = bits if nat.is_device_tensor(ts.samples) else bits.cpu().numpy().view(np.uint32)
+    fps = FingerprintSet(d=params.d, top_k=params.top_k, window_len_s=params.window_len_s,
+                         window_lag_s=params.window_lag_s, indices=indices, epochs=epochs,
+                         bits=out_bits,
+                         meta={"station": ts.station_id, "channel": ts.channel_id,
+                               "sample_rate_hz": ts.sample_rate_hz,
+                               "start_epoch_s": ts.start_epoch_s})
+    return fps, stats

@@ -1,0 +1,166 @@
+"""Fingerprint chain parity on the GPU.
+
+Tolerances (north star): spectrogram and wavelet values within 1e-4 relative
+(with an absolute floor of 1e-4 * max|ref| for near-zero detail
+coefficients); binary fingerprints agree on >= 99.9% of bits.  Mirrors the
+reference's tests/test_fingerprint.py strategy (Haar oracle + roundtrip,
+resize constants, top-K oracle with ties and sign encoding, MAD definition,
+error taxonomy) plus golden vectors produced by the reference itself."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import fingerprint as ofp
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def fp():
+    from paper_1803_09835_b200 import fingerprint
+    return fingerprint
+
+
+def _params(fp, p):
+    return fp.FingerprintParams(window_len_s=p["window_len_s"], window_lag_s=p["window_lag_s"],
+                                freq_bins=p["freq_bins"], time_bins=p["time_bins"],
+                                top_k=p["top_k"], band_low_hz=p["band_low_hz"],
+                                band_high_hz=p["band_high_hz"],
+                                stft=fp.StftParams(p["frame_len_s"], p["hop_s"]))
+
+
+def _close(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    atol = RTOL * max(1.0, float(np.abs(want).max()))
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=atol)
+
+
+def _ts(x, sr=100.0, start=0.0):
+    from paper_1803_09835_b200.ingest import TimeSeries
+    return TimeSeries("ST0", "HHZ", sr, start, x)
+
+
+def test_golden_cfg0_chain(fp, golden_fingerprint):
+    from paper_1803_09835_b200 import workloads
+    case = golden_fingerprint["cfg0_half_hour"]
+    params = _params(fp, workloads.CFG0_PARAMS)
+    ts = _ts(case["samples"], start=1000.0)
+    freqs, times, logpow = fp.spectrogram(ts, params)
+    r0, r1 = (int(v) for v in case["band_rows"])
+    _close(logpow[r0:r1].T, case["band"])
+    exact = np.mean(logpow[r0:r1].T == case["band"])
+    assert exact > 0.999
+    (idx, ep, imgs), = list(fp.iter_image_batches(ts, params, indices=case["sel"]))
+    _close(imgs, case["images"])
+    (idx, ep, coeffs), = list(fp.iter_coeff_batches(ts, params, indices=case["sel"]))
+    _close(coeffs, case["coeffs"])
+    assert np.array_equal(idx, case["sel"]) and np.allclose(ep, 1000.0 + case["sel"] * 1.0)
+    fps, mad = fp.fingerprint_series(ts, params, mad_rate=0.1, mad_seed=0)
+    assert (mad.n_sampled, mad.n_total) == tuple(int(v) for v in case["meta"])
+    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(mad.mad, case["mad"], rtol=1e-5, atol=1e-7)
+    assert np.array_equal(mad.mad > 0, case["mad"] > 0)  # the structural zero-MAD coefficients
+    assert fps.bits.shape == case["bits"].shape and fps.bits.dtype == np.uint32
+    assert np.mean(fps.bits == case["bits"]) >= 0.999
+    fps.validate()
+    assert fps.meta["station"] == "ST0" and fps.d == 4096
+
+
+def test_golden_small_full_band(fp, golden_fingerprint):
+    case = golden_fingerprint["small_full_band"]
+    params = fp.FingerprintParams(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=12,
+                                  top_k=24, stft=fp.StftParams(frame_len_s=0.5, hop_s=0.05))
+    fps, mad = fp.fingerprint_series(_ts(case["samples"]), params, mad_rate=1.0)
+    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-5, atol=1e-7)
+    assert np.mean(fps.bits == case["bits"]) >= 0.999
+
+
+def test_random_traces_vs_oracle(fp):
+    rng = np.random.default_rng(11)
+    for n, params in [(20_000, dict(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=16,
+                                    top_k=24, band_low_hz=None, band_high_hz=None,
+                                    frame_len_s=0.5, hop_s=0.05)),
+                      (9_000, dict(window_len_s=4.0, window_lag_s=0.7, freq_bins=6, time_bins=10,
+                                   top_k=9, band_low_hz=3.0, band_high_hz=20.0,
+                                   frame_len_s=0.64, hop_s=0.13))]:
+        x = rng.standard_normal(n)  # float64 trace
+        res = ofp.fingerprint(x, 100.0, params, mad_rate=0.5, mad_seed=3)
+        fps, mad = fp.fingerprint_series(_ts(x), _params(fp, params), mad_rate=0.5, mad_seed=3)
+        np.testing.assert_allclose(mad.median, res["median"], rtol=1e-5, atol=1e-7)
+        assert np.mean(fps.bits == res["bits"]) >= 0.999
+
+
+def test_haar_matches_oracle_and_roundtrip(fp):
+    rng = np.random.default_rng(5)
+    for shape in [(2, 2), (4, 4), (8, 2), (2, 8), (4, 6), (3, 8), (32, 128), (5, 7, 12)]:
+        a = rng.standard_normal(shape)
+        np.testing.assert_allclose(fp.haar2d(a), ofp.haar2d(a), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(fp.ihaar2d(fp.haar2d(a)), a, rtol=1e-9, atol=1e-9)
+    c = fp.haar2d(np.full((32, 128), 1.5))
+    assert c[0, 0] == pytest.approx(1.5 * math.sqrt(32 * 128), rel=1e-12)
+    from paper_1803_09835_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        fp.haar2d(np.zeros(4))
+
+
+def test_topk_oracle_ties_and_signs(fp):
+    rng = np.random.default_rng(2)
+    n = 64
+    med = rng.standard_normal(n)
+    mad = np.abs(rng.standard_normal(n)) + 0.1
+    mad[[3, 10, 40]] = 0.0  # ineligible
+    stats = fp.MadStats(median=med, mad=mad, rate=1.0, seed=0, n_sampled=1, n_total=1)
+    c = rng.standard_normal((50, n)).astype(np.float32)
+    # engineered ties: several coefficients at the same |v'|
+    c[:, 20] = (med[20] + 1.5 * mad[20]).astype(np.float32)
+    c[:, 21] = (med[21] - 1.5 * mad[21]).astype(np.float32)
+    c[:5] = np.float32(0.0)
+    for k in (1, 7, 30, 61):
+        got = fp.topk_bits(c, stats, k)
+        want = ofp.topk_bits(c, med, mad, k)
+        assert np.array_equal(got, want), k
+    scores = fp.normalize(c, stats)
+    want = np.where(mad > 0, (c.astype(np.float64) - med) / np.where(mad > 0, mad, 1.0), 0.0)
+    np.testing.assert_allclose(scores, want, rtol=1e-15, atol=0)
+
+
+def test_errors(fp):
+    from paper_1803_09835_b200.errors import DataError, ParameterError
+    params = fp.FingerprintParams(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=16,
+                                  top_k=24, stft=fp.StftParams(frame_len_s=0.5, hop_s=0.05))
+    with pytest.raises(DataError):
+        fp.fingerprint_series(_ts(np.zeros(100)), params)
+    with pytest.raises(ParameterError):
+        fp.FingerprintParams(top_k=0).validate()
+    stats = fp.MadStats(median=np.zeros(4), mad=np.array([1.0, 0.0, 0.0, 0.0]), rate=1.0, seed=0,
+                        n_sampled=1, n_total=1)
+    with pytest.raises(ParameterError):
+        fp.topk_bits(np.zeros((1, 4)), stats, 2)
+    with pytest.raises(DataError):
+        fp.topk_bits(np.array([[np.nan, 0, 0, 0]]), stats, 1)
+
+
+def test_device_trace_and_search_integration(fp):
+    import torch
+    from oracle import minmax as omm
+    from oracle import search as osr
+    from paper_1803_09835_b200 import lsh_search as ls
+    from paper_1803_09835_b200 import workloads
+    x, _ = workloads.cfg0_trace(n_samples=90_000, seed=9, copies=3)
+    params = _params(fp, workloads.CFG0_PARAMS)
+    fps_h, mad = fp.fingerprint_series(_ts(x), params)
+    fps_d, _ = fp.fingerprint_series(_ts(torch.from_numpy(x).cuda()), params)
+    assert fps_d.bits.is_cuda
+    assert np.array_equal(fps_d.bits.cpu().numpy().view(np.uint32), fps_h.bits)
+    cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, occurrence_threshold=0.01)
+    rec, st, mapping = ls.search_fingerprints(fps_h, cfg)
+    sigs = omm.signatures_c(fps_h.bits, mapping.values, 100, 2, threads=4)
+    want, wst = osr.search(sigs, tables=100, min_matches=5, partitions=1,
+                           occurrence_threshold=0.01, exclusion_windows=10)
+    assert rec.tobytes() == want.tobytes()
+    assert st.distinct_pairs == wst["distinct_pairs"]
