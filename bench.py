@@ -53,7 +53,28 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--group-frac", type=float, default=1 / 400, help="noise-group density (design experiments)")
+    ap.add_argument("--no-fingerprint", action="store_true")
+    ap.add_argument("--shard", default="tables", choices=["tables", "stations"],
+                    help="N>1: one station's search table-sharded over the ranks (strong scaling, "
+                         "north star) or one independent station per rank (weak scaling)")
+    ap.add_argument("--fp-samples", type=int, default=8_640_000)
     return ap.parse_args()
+
+
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def measured_traffic(n):
+    """DRAM bytes (read + write) of the pair stage per step, from the committed
+    `ncu --set full` capture summary (profiles/traffic.json), or None."""
+    try:
+        with open(TRAFFIC_PATH) as f:
+            t = json.load(f)
+        if int(t["n"]) != n:
+            return None
+        return float(sum(t["pair_stage_dram_bytes"].values())), t["source"]
+    except Exception:
+        return None
 
 
 def peaks():
@@ -171,6 +192,46 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- fingerprinting
+
+def fingerprint_bench(n_samples, steps, device):
+    """Second BASELINE metric: fingerprint Msamples/s (fingerprint_series on a
+    device-resident cfg0-style trace: STFT + MAD sample + main pass)."""
+    import torch
+    from paper_1803_09835_b200 import fingerprint as fp
+    from paper_1803_09835_b200 import workloads
+    from paper_1803_09835_b200.ingest import TimeSeries
+    x, _ = workloads.cfg0_trace(n_samples=n_samples, seed=0)
+    xd = torch.from_numpy(x).to(device)
+    p = workloads.CFG0_PARAMS
+    params = fp.FingerprintParams(window_len_s=p["window_len_s"], window_lag_s=p["window_lag_s"],
+                                  freq_bins=p["freq_bins"], time_bins=p["time_bins"], top_k=p["top_k"],
+                                  band_low_hz=p["band_low_hz"], band_high_hz=p["band_high_hz"],
+                                  stft=fp.StftParams(p["frame_len_s"], p["hop_s"]))
+    ts = TimeSeries("ST0", "HHZ", workloads.SR_HZ, 0.0, xd)
+    fp.fingerprint_series(ts, params, mad_rate=0.1)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fps, mad = fp.fingerprint_series(ts, params, mad_rate=0.1)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    # e2e: host float32 numpy trace in, host bits out
+    tsh = TimeSeries("ST0", "HHZ", workloads.SR_HZ, 0.0, x)
+    t0 = time.perf_counter()
+    fph, _ = fp.fingerprint_series(tsh, params, mad_rate=0.1)
+    e2e_s = time.perf_counter() - t0
+    return {"metric": "fingerprint Msamples/s", "value": n_samples / ms / 1e3, "unit": "Msamples/s",
+            "ms_per_step": ms, "n_samples": n_samples, "n_fingerprints": int(len(fps)),
+            "workload": "cfg0 (BASELINE.json configs[0]): 1 day at 100 Hz, 5 chirp templates x 20, "
+                        "window 10 s / lag 1 s, 32x64 images, top-K 200, MAD rate 0.1",
+            "e2e": {"value": n_samples / e2e_s / 1e6, "unit": "Msamples/s",
+                    "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(fph.bits.nbytes)}}
+
+
 # ---------------------------------------------------------------------- ours
 
 def run_ours(args):
@@ -179,9 +240,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # QS_BENCH_BACKEND=gloo lets a 1-GPU box run the N>1 control flow (ranks
+    # share the device; no kernel waits on another rank's kernel)
+    backend = os.environ.get("QS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device(f"cuda:{local}")
     from paper_1803_09835_b200 import lsh_search as ls
     from paper_1803_09835_b200 import minmax_hash as mh
@@ -190,18 +258,37 @@ def run_ours(args):
 
     n = args.n
     occ = args.occ if args.occ > 0 else None
-    bits, _ = workloads.cfg1_bits_torch(n=n, seed=1 + rank, device=dev, group_frac=args.group_frac)
-    torch.cuda.synchronize()
+    tables_mode = world > 1 and args.shard == "tables"
+    # tables mode: every rank generates the same station (seed 1) and keeps only
+    # its block of rows; stations mode: rank r searches its own station
+    bits, _ = workloads.cfg1_bits_torch(n=n, seed=1 if tables_mode else 1 + rank, device=dev,
+                                        group_frac=args.group_frac)
     mapping = mh.gen_hash_mapping(4096, 100, 4, 0)
     mapping.device_plan()
     cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, seed=0, partitions=1,
                           occurrence_threshold=occ)
+    comm = None
+    if tables_mode:
+        from paper_1803_09835_b200 import sharded as sh
+        comm = sh.TorchComm()
+        a, b, s_rows = sh.row_block(n, world, rank)
+        blk = bits[a:b]
+        if b - a < s_rows:
+            blk = torch.cat([blk, blk[:1].expand(s_rows - (b - a), -1)])
+        blk = blk.contiguous()
+        host_rows = (a, b)
+        del bits
+        bits = blk
+    torch.cuda.synchronize()
 
     last = {}
 
     def step(timing=False):
-        keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
-        trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=timing)
+        if tables_mode:
+            trip, st, ds = sh.search_bits_sharded(bits, n, cfg, mapping, 0, comm=comm, timing=timing)
+        else:
+            keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
+            trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=timing)
         last.update(trip=trip, stats=st, ds=ds)
         return ds
 
@@ -226,51 +313,83 @@ def run_ours(args):
         tmax = torch.tensor([ms], device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         ms = float(tmax.item())
-    value = world * n / (ms / 1e3)
+    value = (n if tables_mode else world * n) / (ms / 1e3)
 
     # per-stage split + roofline of the dominant kernel (pair enumeration)
     sig_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     sig_ev[0].record()
-    keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
-    sig_ev[1].record()
-    trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=True)
+    if tables_mode:
+        rkeys, tags, bad = sh.gather_search_layout(bits, n, mapping, comm)
+        sig_ev[1].record()
+        own = sh.shard_tables(100, world, rank)
+        ds = ls.DeviceSearch(sh.own_keys(rkeys, own), rkeys, tags, n, 100, timing=True, tables=own)
+        trip, st, ds = sh.run_search_sharded(ds, comm, n, 100, cfg, 0)
+    else:
+        keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
+        sig_ev[1].record()
+        trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=True)
     torch.cuda.synchronize()
     stages = ds.stage_times_ms()
-    stages["minhash"] = sig_ev[0].elapsed_time(sig_ev[1])
+    stages["minhash" + ("+gather" if tables_mode else "")] = sig_ev[0].elapsed_time(sig_ev[1])
     bs = ds.bsize[: ds.nb].to(torch.int64)
     hits = int((bs * (bs - 1) // 2).sum().item())
     m2 = int(bs.sum().item())
     passes = 2 if occ is not None else 1
-    pair_bytes = passes * (16 * hits + 4 * m2) + 20 * st.emitted_triplets
+    pair_bytes = passes * (16 * hits + 4 * m2) + 20 * (st.emitted_triplets if not tables_mode else 0)
     pair_ms = sum(v for k, v in stages.items() if k.startswith("pairs"))
     hbm, peak_kind = peaks()
     achieved = pair_bytes / (pair_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "k_pairs (first-colliding-table pair enumeration)",
+    traffic = measured_traffic(n) if not tables_mode else None
+    roof = {"bound": "hbm", "kernel": "k_pairs_pc (first-colliding-table pair enumeration)",
             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None,
+            "frac": achieved / hbm, "traffic": traffic[0] if traffic else None,
+            "traffic_source": traffic[1] if traffic else None,
+            "scope": ("all pair-enumeration launches of one step (matched + distinct pass)"
+                      + (f", rank 0's {len(ds.table_ids) if ds.table_ids is not None else 100}"
+                         " tables" if tables_mode else "")),
             "algorithmic_bytes": pair_bytes, "hits": hits, "passes": passes,
             "ms": pair_ms}
 
     e2e = None
     if not args.no_e2e:
-        host_bits = bits.cpu().numpy().view(np.uint32)
+        if tables_mode:
+            a, b = host_rows
+            host_bits = bits[: b - a].cpu().numpy().view(np.uint32)
+        else:
+            host_bits = bits.cpu().numpy().view(np.uint32)
+        rows = host_bits.shape[0]
         fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
-                             indices=np.arange(n, dtype=np.uint64),
-                             epochs=np.arange(n, dtype=np.float64), bits=host_bits)
+                             indices=np.arange(rows, dtype=np.uint64),
+                             epochs=np.arange(rows, dtype=np.float64), bits=host_bits)
         cfg_e = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, seed=0,
                                 occurrence_threshold=occ, near_repeat_exclusion_s=0.0)
-        ls.search_fingerprints(fps, cfg_e, mapping=mapping)
+
+        def e2e_call():
+            if tables_mode:
+                return sh.search_fingerprints_sharded(fps, n, cfg_e, mapping=mapping)
+            return ls.search_fingerprints(fps, cfg_e, mapping=mapping)
+
+        e2e_call()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         out_bytes = 0
         for _ in range(args.e2e_steps):
-            rec, est, _ = ls.search_fingerprints(fps, cfg_e, mapping=mapping)
+            rec, est, _ = e2e_call()
             out_bytes = rec.nbytes
         torch.cuda.synchronize()
         e_s = (time.perf_counter() - t0) / args.e2e_steps
-        e2e = {"value": n / e_s, "unit": "fingerprints/s", "h2d_bytes_per_step": int(host_bits.nbytes),
-               "d2h_bytes_per_step": int(out_bytes), "seconds_per_step": e_s,
-               "path": "lsh_search.search_fingerprints(FingerprintSet with host numpy bits)"}
+        if world > 1:
+            et = torch.tensor([e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e_s = float(et.item())
+        e_units = n if tables_mode else world * n
+        e2e = {"value": e_units / e_s, "unit": "fingerprints/s",
+               "h2d_bytes_per_step": int(e_units * 400 * 4), "d2h_bytes_per_step": int(out_bytes),
+               "seconds_per_step": e_s,
+               "path": ("sharded.search_fingerprints_sharded (host row block per rank)" if tables_mode
+                        else "lsh_search.search_fingerprints(FingerprintSet with host numpy bits)")}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -283,20 +402,29 @@ def run_ours(args):
                           f"{threads} threads ({r['sig_s']:.2f} s) + numpy port of search_signatures "
                           f"single-threaded ({r['search_s']:.2f} s)")}
 
+    fpb = None
+    if rank == 0 and not args.no_fingerprint:
+        fpb = fingerprint_bench(args.fp_samples, max(1, args.steps), dev)
+
     if rank == 0:
         line = {"metric": "LSH search fingerprints/sec (MinHash+bucket+pair-count)",
                 "value": value, "unit": "fingerprints/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": {"workload": "cfg1 (BASELINE.json configs[1])", "n_per_gpu": n,
+                "scaling": "strong" if tables_mode else "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic",
+                "config": {"workload": "cfg1 (BASELINE.json configs[1])",
+                           ("n_total" if tables_mode else "n_per_gpu"): n,
                            "d": 4096, "set_bits": 400, "tables": 100, "hash_funcs": 4,
                            "min_matches": 5, "occurrence_threshold": occ, "partitions": 1,
                            "l2": "inputs (12.8 GB bits) larger than L2; no flush",
-                           "parallelism": f"station-sharded x{world}"},
+                           "parallelism": (f"table-sharded x{world} (round-robin tables, "
+                                           "row-sharded Min-Max + NCCL all-gather)" if tables_mode
+                                           else f"station-sharded x{world}")},
                 "stages_ms": stages, "emitted_triplets": st.emitted_triplets,
                 "filtered_fingerprints": st.filtered_fingerprints,
                 "distinct_pairs": st.distinct_pairs, "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+                "fingerprint": fpb}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

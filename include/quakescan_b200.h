@@ -66,9 +66,11 @@ int qs_minmax_signatures(const uint32_t* bits_dev, uint64_t n, uint32_t K,
 /* Same computation, search layout: keys_dev (t, n) uint64 table-major and
  * rkeys_dev (n, t) uint64 row-major hold mix64(sig) (a bijection of the
  * signature word, so bucket equality is unchanged) and tags_dev
- * (n, ceil(t/32), 16) uint32 the bit-sliced 16-bit tags (plane p of word w =
- * bit p of the tags of tables 32w..32w+31) used for exact
- * first-colliding-table dedup.  sigs_dev (n, t) may be NULL. */
+ * [2][n][ceil(t/32)][8] uint32 the bit-sliced 16-bit tags (plane p of word w
+ * = bit p of the tags of tables 32w..32w+31; planes 0-7 in the first half,
+ * 8-15 in the second) used for exact first-colliding-table dedup.
+ * sigs_dev (n, t) and keys_dev may be NULL (a table-sharded rank rebuilds
+ * its own tables' keys from the gathered rkeys). */
 int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K,
                                 const void* plan_dev, uint32_t d, uint32_t t,
                                 uint32_t k_half, uint64_t* sigs_dev, uint64_t* keys_dev,
@@ -89,7 +91,7 @@ int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
  * The search (lsh_search.search_signatures, lsh_search.py:222-303) runs as the
  * stage sequence below, orchestrated by the Python host layer which owns all
  * buffers.  Layouts: keys (t, n) / rkeys (n, t) uint64 mixed signature words;
- * tags (n, W, 16) uint32, W = ceil(t/32).  A bucket list is (bstart = offset
+ * tags [2][n][W][8] uint32, W = ceil(t/32).  A bucket list is (bstart = offset
  * of the bucket's first member in the member-id array, bsize, btab = table). */
 
 /* Row-major signatures (n, t) -> keys + rkeys + tags.  Used when the caller
@@ -108,11 +110,15 @@ int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t,
 /* Bucket listing (lsh_search.py:167-172 run lengths): non-singleton buckets
  * of all tables.  Call first with bstart_dev == NULL: counts_dev[0] = number
  * of non-singleton buckets, counts_dev[1] = number of buckets (all tables);
- * then with arrays of that capacity to fill them. */
+ * then with arrays of that capacity to fill them.  btab_dev receives each
+ * bucket's table: table_ids_dev[local table] when table_ids_dev is given (a
+ * table-sharded rank passes the global ids of its tables), else the local
+ * index. */
 size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t);
 int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t,
                         uint64_t* bstart_dev, uint32_t* bsize_dev, uint32_t* btab_dev,
-                        uint64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+                        const uint32_t* table_ids_dev, uint64_t* counts_dev, void* ws_dev,
+                        size_t ws_bytes, void* stream);
 
 /* SearchStats bucket fields (lsh_search.py:70-109, 295-302): lookups_total
  * (counted before the canonical/dt/exclusion masks, :192-194), the sizes of
@@ -168,6 +174,20 @@ int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_
                              uint64_t n_pairs, uint64_t n, double threshold,
                              const uint64_t* edges_dev, uint32_t p, uint8_t* excluded_dev,
                              unsigned long long* counters_dev, void* ws_dev, void* stream);
+
+/* The same filter in three steps, for table-sharded searches whose matched
+ * pairs are spread over ranks: (1) degree_dev (n uint32, zeroed by the caller)
+ * += within-partition matched-pair degrees — sum it over ranks; (2) mark:
+ * excluded_dev = 2 for core, 1 for matched neighbours of core, else 0 — take
+ * the elementwise max over ranks; (3) finish: normalise to 0/1 and
+ * counters_dev[0] += number excluded. */
+int qs_lsh_occ_degree(const uint64_t* pair_key_dev, uint64_t n_pairs, const uint64_t* edges_dev,
+                      uint32_t p, uint32_t* degree_dev, void* stream);
+int qs_lsh_occ_mark(const uint64_t* pair_key_dev, uint64_t n_pairs, const uint32_t* degree_dev,
+                    uint64_t n, double threshold, const uint64_t* edges_dev, uint32_t p,
+                    uint8_t* excluded_dev, void* stream);
+int qs_lsh_occ_finish(uint8_t* excluded_dev, uint64_t n, unsigned long long* counters_dev,
+                      void* stream);
 
 /* Matched pairs that survive the exclusion rule (pass-2 emission of
  * lsh_search.py:276-287), appended to out_* with *counter_dev as cursor. */

@@ -286,12 +286,14 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
 
 // bsize holds in-table tail positions on entry, bucket sizes on exit
 __global__ void k_make_sizes(const uint64_t* __restrict__ heads, const uint64_t* __restrict__ nbp,
-                             uint64_t n, uint32_t* __restrict__ bsize, uint32_t* __restrict__ btab) {
+                             uint64_t n, uint32_t* __restrict__ bsize, uint32_t* __restrict__ btab,
+                             const uint32_t* __restrict__ table_ids) {
     const uint64_t nb = *nbp;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         bsize[i] = (uint32_t)(bsize[i] - heads[i] % n + 1);
-        btab[i] = (uint32_t)(heads[i] / n);
+        const uint32_t local = (uint32_t)(heads[i] / n);
+        btab[i] = table_ids ? table_ids[local] : local;
     }
 }
 
@@ -572,8 +574,8 @@ size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t) {
 }
 
 int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint64_t* bstart_dev,
-                        uint32_t* bsize_dev, uint32_t* btab_dev, uint64_t* counts_dev,
-                        void* ws_dev, size_t ws_bytes, void* stream) {
+                        uint32_t* bsize_dev, uint32_t* btab_dev, const uint32_t* table_ids_dev,
+                        uint64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     QS_ARG(ws_bytes >= qs_lsh_list_ws_bytes(n, t), "list workspace too small");
     const uint64_t total = n * t;
@@ -602,7 +604,7 @@ int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint6
         k_list_write<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, kind, cnt, bstart_dev,
                                                  bsize_dev);
     }
-    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev, btab_dev);
+    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev, btab_dev, table_ids_dev);
     QS_CHECK_LAUNCH("list buckets");
     return QS_OK;
 }
@@ -652,6 +654,36 @@ int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
     return QS_OK;
 }
 
+int qs_lsh_occ_degree(const uint64_t* pair_key_dev, uint64_t n_pairs, const uint64_t* edges_dev,
+                      uint32_t p, uint32_t* degree_dev, void* stream) {
+    if (n_pairs == 0) return QS_OK;
+    k_occ_degree<<<qs_blocks(n_pairs, 256), 256, 0, (cudaStream_t)stream>>>(pair_key_dev, n_pairs,
+                                                                           edges_dev, p, degree_dev);
+    QS_CHECK_LAUNCH("k_occ_degree");
+    return QS_OK;
+}
+
+int qs_lsh_occ_mark(const uint64_t* pair_key_dev, uint64_t n_pairs, const uint32_t* degree_dev,
+                    uint64_t n, double threshold, const uint64_t* edges_dev, uint32_t p,
+                    uint8_t* excluded_dev, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) return QS_OK;
+    k_occ_core<<<qs_blocks(n, 256), 256, 0, st>>>(degree_dev, n, threshold, edges_dev, p, excluded_dev);
+    if (n_pairs)
+        k_occ_touch<<<qs_blocks(n_pairs, 256), 256, 0, st>>>(pair_key_dev, n_pairs, edges_dev, p,
+                                                             excluded_dev);
+    QS_CHECK_LAUNCH("occurrence mark");
+    return QS_OK;
+}
+
+int qs_lsh_occ_finish(uint8_t* excluded_dev, uint64_t n, unsigned long long* counters_dev,
+                      void* stream) {
+    if (n == 0) return QS_OK;
+    k_occ_finish<<<qs_blocks(n, 256), 256, 0, (cudaStream_t)stream>>>(excluded_dev, n, counters_dev);
+    QS_CHECK_LAUNCH("k_occ_finish");
+    return QS_OK;
+}
+
 int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
                              uint64_t n_pairs, uint64_t n, double threshold,
                              const uint64_t* edges_dev, uint32_t p, uint8_t* excluded_dev,
@@ -661,14 +693,11 @@ int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_
     if (n == 0) return QS_OK;
     uint32_t* deg = (uint32_t*)ws_dev;
     QS_CUDA(cudaMemsetAsync(deg, 0, n * 4, st), "memset");
-    if (n_pairs)
-        k_occ_degree<<<qs_blocks(n_pairs, 256), 256, 0, st>>>(pair_key_dev, n_pairs, edges_dev, p, deg);
-    k_occ_core<<<qs_blocks(n, 256), 256, 0, st>>>(deg, n, threshold, edges_dev, p, excluded_dev);
-    if (n_pairs)
-        k_occ_touch<<<qs_blocks(n_pairs, 256), 256, 0, st>>>(pair_key_dev, n_pairs, edges_dev, p, excluded_dev);
-    k_occ_finish<<<qs_blocks(n, 256), 256, 0, st>>>(excluded_dev, n, counters_dev);
-    QS_CHECK_LAUNCH("occurrence filter");
-    return QS_OK;
+    int rc = qs_lsh_occ_degree(pair_key_dev, n_pairs, edges_dev, p, deg, stream);
+    if (rc) return rc;
+    rc = qs_lsh_occ_mark(pair_key_dev, n_pairs, deg, n, threshold, edges_dev, p, excluded_dev, stream);
+    if (rc) return rc;
+    return qs_lsh_occ_finish(excluded_dev, n, counters_dev, stream);
 }
 
 int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev, uint64_t n_pairs,

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) k_signatures(
             if (SEARCH) {
                 const uint64_t key = mix_key(acc);
                 if (i < t) {
-                    keys[(uint64_t)i * n + row] = key;
+                    if (keys) keys[(uint64_t)i * n + row] = key;
                     rkeys[row * t + i] = key;
                 }
                 const uint32_t tag = (uint32_t)key & 0xFFFFu;

@@ -141,15 +141,27 @@ class DeviceSearch:
     """Device buffers + launches of one search over the search layout.
 
     keys: (t, n) int64 table-major, rkeys: (n, t) int64 row-major (mix64 of
-    the signature words), tags: (n, ceil(t/32), 16) int32 CUDA tensors.
-    Records per-stage CUDA event times when `timing` is set (bench.py)."""
+    the signature words), tags: (2, n, ceil(t/32), 8) int32 CUDA tensors.
+    `tables` (optional, ascending global table ids) restricts the buckets to
+    those tables — one rank's share of a table-sharded search (sharded.py);
+    `keys` then holds either all t tables or only these rows.  rkeys/tags
+    always cover all t tables (the first-colliding-table rule looks at every
+    earlier table).  Records per-stage CUDA event times when `timing` is set."""
 
     MODE_FULL, MODE_MATCHED, MODE_DISTINCT = 0, 1, 2
 
-    def __init__(self, keys, rkeys, tags, n: int, t: int, timing: bool = False):
+    def __init__(self, keys, rkeys, tags, n: int, t: int, timing: bool = False, tables=None):
         self.torch = nat.torch()
-        self.keys, self.rkeys, self.tags, self.n, self.t = keys, rkeys, tags, n, t
+        self.rkeys, self.tags, self.n, self.t = rkeys, tags, n, t
         self.dev = keys.device
+        self.table_ids = None
+        if tables is not None and list(tables) != list(range(t)):
+            ids = self.torch.as_tensor(list(tables), dtype=self.torch.int64)
+            if keys.shape[0] != len(ids):
+                keys = keys.index_select(0, ids.to(self.dev))
+            self.table_ids = ids.to(self.torch.int32).to(self.dev)
+        self.keys = keys
+        self.kt = int(keys.shape[0])
         self.timing = timing
         self.events = []
         self.launches = 0
@@ -170,7 +182,7 @@ class DeviceSearch:
         return self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.dev)
 
     def buckets(self):
-        torch, n, t = self.torch, self.n, self.t
+        torch, n, t = self.torch, self.n, self.kt
         lib = nat.lib()
         self._mark("buckets")
         skeys = torch.empty((t, n), dtype=torch.int64, device=self.dev)
@@ -183,8 +195,8 @@ class DeviceSearch:
         self._mark("list")
         lws = self._empty(lib.qs_lsh_list_ws_bytes(n, t))
         counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
-        nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, None, None, None, nat.ptr(counts),
-                 nat.ptr(lws), lws.numel(), nat.stream())
+        nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, None, None, None, None,
+                 nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
         nb, heads = (int(v) for v in counts.tolist())
         self.nb, self.heads = nb, heads
         self.bstart = torch.empty(max(nb, 1), dtype=torch.int64, device=self.dev)
@@ -192,8 +204,8 @@ class DeviceSearch:
         self.btab = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         if nb:
             nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, nat.ptr(self.bstart),
-                     nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(counts), nat.ptr(lws),
-                     lws.numel(), nat.stream())
+                     nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(self.table_ids),
+                     nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
         self.launches += 2 * 4 + 2 * 5 + 1
         self.full = (self.sids, self.bstart, self.bsize, self.btab, self.nb)
 
@@ -202,7 +214,7 @@ class DeviceSearch:
         torch, lib = self.torch, nat.lib()
         self._mark("compact")
         nb = self.nb
-        sids2 = torch.empty(max(1, self.n * self.t), dtype=torch.int32, device=self.dev)
+        sids2 = torch.empty(max(1, self.n * self.kt), dtype=torch.int32, device=self.dev)
         bstart2 = torch.empty(max(nb, 1), dtype=torch.int64, device=self.dev)
         bsize2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         btab2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
@@ -256,6 +268,29 @@ class DeviceSearch:
                  nat.stream())
         self.launches += 4
         return emask, int(cnt.item())
+
+    # the occurrence filter in three steps (table-sharded searches reduce the
+    # degree vector with SUM and the mark vector with MAX between them)
+    def occ_degree(self, pk, matched, edges, p):
+        self._mark("filter")
+        deg = self.torch.zeros(self.n, dtype=self.torch.int32, device=self.dev)
+        nat.call("qs_lsh_occ_degree", nat.ptr(pk), matched, nat.ptr(edges), p, nat.ptr(deg),
+                 nat.stream())
+        self.launches += 1
+        return deg
+
+    def occ_mark(self, pk, matched, deg, threshold, edges, p):
+        mark = self.torch.empty(self.n, dtype=self.torch.uint8, device=self.dev)
+        nat.call("qs_lsh_occ_mark", nat.ptr(pk), matched, nat.ptr(deg), self.n, float(threshold),
+                 nat.ptr(edges), p, nat.ptr(mark), nat.stream())
+        self.launches += 2
+        return mark
+
+    def occ_finish(self, mark):
+        cnt = self.torch.zeros(1, dtype=self.torch.int64, device=self.dev)
+        nat.call("qs_lsh_occ_finish", nat.ptr(mark), self.n, nat.ptr(cnt), nat.stream())
+        self.launches += 1
+        return mark, int(cnt.item())
 
     def filter_pairs(self, pk, ps, matched, emask, edges, p):
         torch = self.torch
@@ -356,7 +391,12 @@ def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_w
                 _, _, _, distinct = ds.pairs(ds.MODE_DISTINCT, m, excl, emask, edges, p)
     looks, pieces, mx, hist, big = ds.bucket_stats(emask, edges, p)
     trip = ds.finalize(pk, ps, matched)
-    singles = ds.heads - ds.nb
+    fill_stats(stats, n, t, looks, pieces, mx, hist, big, ds.heads - ds.nb, distinct, matched, n_ex)
+    return trip, stats, ds
+
+
+def fill_stats(stats, n, t, looks, pieces, mx, hist, big, singles, distinct, matched, n_ex):
+    """SearchStats fields (lsh_search.py:295-302) from bucket-walk totals."""
     stats.lookups_total = looks
     stats.distinct_pairs = distinct
     stats.emitted_triplets = matched
@@ -364,10 +404,10 @@ def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_w
     stats.n_queries = n - n_ex
     stats.n_buckets = pieces + singles
     stats.max_bucket = max(mx, 1 if singles else 0)
-    hist = hist.copy()
+    hist = np.array(hist, dtype=np.int64, copy=True)
     hist[1] += singles
     stats.top_bucket_mass = _top_mass(hist, big, stats.n_buckets, n * t)
-    return trip, stats, ds
+    return stats
 
 
 def _empty_triplets():
@@ -404,19 +444,52 @@ def search_signatures(sigs, cfg: SearchConfig, exclusion_windows: int = 0):
                 torch.empty(0, dtype=torch.uint8, device=sigs.device)), stats
     if not on_device:
         sdev = torch.from_numpy(arr.view(np.int64)).to("cuda")
-    W = (t + 31) // 32
-    keys = torch.empty((t, n), dtype=torch.int64, device=sdev.device)
-    rkeys = torch.empty((n, t), dtype=torch.int64, device=sdev.device)
-    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=sdev.device)
-    nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
-             nat.stream())
+    keys, rkeys, tags = prep_signatures(sdev)
     trip, stats, _ = run_search(keys, rkeys, tags, n, t, cfg, exclusion_windows)
     if on_device:
         return trip, stats
     return trip.cpu().numpy().view(TRIPLET_DTYPE), stats
 
 
-def signatures_for_search(bits, mapping: HashMapping):
+def prep_signatures(sdev):
+    """Search layout (keys, rkeys, tags) of a CUDA int64 (n, t) signature matrix."""
+    torch = nat.torch()
+    n, t = (int(v) for v in sdev.shape)
+    W = (t + 31) // 32
+    keys = torch.empty((t, n), dtype=torch.int64, device=sdev.device)
+    rkeys = torch.empty((n, t), dtype=torch.int64, device=sdev.device)
+    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=sdev.device)
+    nat.call("qs_lsh_prep", nat.ptr(sdev), n, t, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
+             nat.stream())
+    return keys, rkeys, tags
+
+
+def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
+    """Host -> device copy through two pinned staging buffers (DMA of chunk i
+    overlaps the host memcpy of chunk i + 1); pageable numpy input."""
+    torch = nat.torch()
+    flat = arr.reshape(-1)
+    out = torch.empty(arr.shape, dtype=torch.from_numpy(flat[:0]).dtype, device="cuda")
+    if flat.size == 0:
+        return out
+    dst = out.view(-1)
+    per = max(1, chunk_bytes // flat.itemsize)
+    stage = [torch.empty(per, dtype=dst.dtype).pin_memory() for _ in range(2)]
+    done = [None, None]
+    for k, a in enumerate(range(0, flat.size, per)):
+        b = min(flat.size, a + per)
+        s = k & 1
+        if done[s] is not None:
+            done[s].synchronize()
+        stage[s][: b - a].numpy()[:] = flat[a:b]
+        dst[a:b].copy_(stage[s][: b - a], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        done[s] = ev
+    return out
+
+
+def signatures_for_search(bits, mapping: HashMapping, with_keys: bool = True):
     """Fused Min-Max kernel writing table-major keys + tags directly (no
     row-major signature round trip). bits: CUDA int32 (n, K)."""
     torch = nat.torch()
@@ -424,7 +497,7 @@ def signatures_for_search(bits, mapping: HashMapping):
     t = mapping.t
     W = (t + 31) // 32
     _, plan = mapping.device_plan()
-    keys = torch.empty((t, n), dtype=torch.int64, device=bits.device)
+    keys = torch.empty((t, n), dtype=torch.int64, device=bits.device) if with_keys else None
     rkeys = torch.empty((n, t), dtype=torch.int64, device=bits.device)
     tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=bits.device)
     bad = torch.zeros(1, dtype=torch.int32, device=bits.device)
@@ -458,9 +531,9 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
             raise ParameterError("bits must be a 2-D (n, K) array")
         if arr.shape[1] < 1:
             raise ParameterError("fingerprints must have at least one set bit")
-        if arr.shape[0] and int(arr.max()) >= mapping.d:
-            raise ParameterError("fingerprint bit index out of range for mapping")
-        bdev = torch.from_numpy(arr.view(np.int32)).to("cuda")
+        # the range check (minmax_hash.py:107-108) runs on the device, flagged by
+        # the signature kernel, instead of a host pass over the whole array
+        bdev = _to_device_staged(arr.view(np.int32))
     n, K = bdev.shape
     if K < 1:
         raise ParameterError("fingerprints must have at least one set bit")
@@ -471,7 +544,7 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
         empty = _empty_triplets() if not on_device else torch.empty(0, dtype=torch.uint8, device="cuda")
         return empty, SearchStats(n_fingerprints=0), mapping
     keys, rkeys, tags, bad = signatures_for_search(bdev, mapping)
-    if on_device and int(bad.item()):
+    if int(bad.item()):
         raise ParameterError("fingerprint bit index out of range for mapping")
     trip, stats, _ = run_search(keys, rkeys, tags, n, cfg.tables, cfg, excl)
     if on_device:
