@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=8_000_000)
+    ap.add_argument("--fingerprints", dest="n", type=int, default=8_000_000)
     ap.add_argument("--occ", type=float, default=1.5e-5, help="occurrence threshold (<=0: off)")
     ap.add_argument("--ref-n", type=int, default=50_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")

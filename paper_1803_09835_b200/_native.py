@@ -11,7 +11,8 @@ import os
 from .errors import DataError, ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libquakescan_b200.so")
+# QS_LIB_PATH: an alternative build of the same library (kernel-configuration sweeps)
+LIB_PATH = os.environ.get("QS_LIB_PATH") or os.path.join(HERE, "lib", "libquakescan_b200.so")
 
 QS_OK, QS_ERR_ARG, QS_ERR_OOM, QS_ERR_CUDA, QS_ERR_DATA = 0, 1, 2, 3, 4
 

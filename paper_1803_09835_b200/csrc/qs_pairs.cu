@@ -36,11 +36,18 @@
 namespace qs {
 
 constexpr int QCAP = 64;
-// Occupancy configuration (measured on B200 at cfg1): 4 CTAs per
-// SM, each 1 producer + 3 consumer warps with two 22 KB staged items.
+// Occupancy configuration (measured on B200 at cfg1, tools/sweep_pairs.py):
+// 1 producer + 3 consumer warps per CTA; MATCHED rows (8 planes) run 5 CTAs/SM
+// with two 16 KB staged buffers, the 16-plane modes 4 CTAs/SM with 21 KB.
 #ifndef QS_CWARPS
 #define QS_CWARPS 3
-#define QS_BUFKB 22
+#endif
+#ifndef QS_BUFKB_M
+#define QS_BUFKB_M 16
+#define QS_MINB_M 5
+#endif
+#ifndef QS_BUFKB
+#define QS_BUFKB 21
 #define QS_MINB 4
 #endif
 #ifndef QS_NBUF
@@ -48,8 +55,16 @@ constexpr int QCAP = 64;
 #endif
 constexpr int NBUF = QS_NBUF;          // staged items in flight per CTA (ring)
 constexpr int CWARPS = QS_CWARPS;      // consumer warps per CTA (+1 producer warp)
-constexpr int PTHREADS = (CWARPS + 1) * 32;
-constexpr uint32_t BPIECE = 64;        // B rows per chunk
+#ifndef QS_NPROD
+#define QS_NPROD 1
+#endif
+constexpr int NPROD = QS_NPROD;        // producer warps; producer p stages items k = p mod NPROD
+static_assert(NPROD == 1 || NBUF % NPROD == 0, "each producer needs its own buffers");
+constexpr int PTHREADS = (CWARPS + NPROD) * 32;
+#ifndef QS_BPIECE
+#define QS_BPIECE 16
+#endif
+constexpr uint32_t BPIECE = QS_BPIECE;  // B rows per chunk
 constexpr uint32_t NCH_DONE = 0xFFFFFFFFu;
 enum { MODE_FULL = 0, MODE_MATCHED = 1, MODE_DISTINCT = 2 };
 
@@ -72,15 +87,21 @@ struct TileCfg {
     static constexpr int ROW = W * NP;                        // u32 per staged row
     static constexpr int ROWP = ROW + 4;                      // padded stride: row-parallel
                                                               // 16-byte loads are conflict-free
-    static constexpr int CAP = (QS_BUFKB * 1024) / (ROWP * 4);  // rows per buffer
+    static constexpr int BUFKB = MODE == MODE_MATCHED ? QS_BUFKB_M : QS_BUFKB;
+    static constexpr int MINB = MODE == MODE_MATCHED ? QS_MINB_M : QS_MINB;
+    static constexpr int CAP = (BUFKB * 1024) / (ROWP * 4);  // rows per buffer
     static constexpr int L = CAP / 2;                         // small-bucket / segment limit
-    static constexpr int MAXCH = L + (L / 32 + 1) * (L / 64 + 2) + 16;
+    static constexpr int MAXCH = L + (2 * L / 32 + 1) * (2 * L / (int)BPIECE + 1) + 16;
     static constexpr int QWORDS = QCAP * (3 + W);
-    // per buffer: rows, ids, chunk descriptors
+    // NBUF staged tag-row buffers + NMETA = NBUF + 1 item descriptors (member ids,
+    // chunk list): the producer writes item k+1's descriptor while item k's rows
+    // are in flight, so only one memory round trip separates "buffer free" from
+    // "buffer full".
+    static constexpr int NMETA = NBUF + NPROD;
     static constexpr size_t IDS_BYTES = ((size_t)CAP * 4 + 15) & ~(size_t)15;
-    static constexpr size_t BUF =
-        (((size_t)CAP * ROWP * 4 + IDS_BYTES + (size_t)MAXCH * 8) + 127) & ~(size_t)127;
-    static constexpr size_t SMEM = NBUF * BUF + (size_t)CWARPS * QWORDS * 4 + 128;
+    static constexpr size_t ROWBUF = ((size_t)CAP * ROWP * 4 + 127) & ~(size_t)127;
+    static constexpr size_t META = ((IDS_BYTES + (size_t)MAXCH * 8) + 127) & ~(size_t)127;
+    static constexpr size_t SMEM = NBUF * ROWBUF + NMETA * META + (size_t)CWARPS * QWORDS * 4 + 128;
 };
 
 // ------------------------------------------------------------ primitives
@@ -283,27 +304,27 @@ struct Plan {
 };
 
 template <int W, int MODE, bool HAS_E>
-__global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
+__global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
     const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
     const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab, Plan plan,
     const uint64_t* __restrict__ rkeys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
     uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges,
     uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
-    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work) {
+    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work, uint32_t tmax) {
     using C = TileCfg<W, MODE>;
     constexpr int NP = C::NP;
     constexpr uint32_t L = C::L;
     extern __shared__ __align__(128) unsigned char psm[];
     __shared__ __align__(8) uint64_t full_bar[NBUF], empty_bar[NBUF];
-    __shared__ uint32_t s_nch[NBUF], s_next[NBUF];
+    __shared__ uint32_t s_nch[C::NMETA], s_next[C::NMETA], s_nrows[C::NMETA];
     // producer scratch: tile bucket metadata, small-bucket offsets / member-list starts
-    __shared__ uint64_t m_mpre[L + 1], m_bstart[L], p_st[L];
-    __shared__ uint32_t m_bsize[L], m_btab[L], p_off[L + 1];
-    // buffer b: rows | ids | chunk descriptors
-    auto rowsb = [&](int b) { return (uint32_t*)(psm + b * C::BUF); };
-    auto idsb = [&](int b) { return (uint32_t*)(psm + b * C::BUF + (size_t)C::CAP * C::ROWP * 4); };
-    auto chb = [&](int b) {
-        return (uint2*)(psm + b * C::BUF + (size_t)C::CAP * C::ROWP * 4 + C::IDS_BYTES);
+    __shared__ uint64_t p_st_all[NPROD][L];
+    __shared__ uint32_t p_off_all[NPROD][L + 1];
+    // rows buffer b | item descriptor a: member ids, chunk descriptors
+    auto rowsb = [&](int b) { return (uint32_t*)(psm + b * C::ROWBUF); };
+    auto idsm = [&](int a) { return (uint32_t*)(psm + NBUF * C::ROWBUF + a * C::META); };
+    auto chm = [&](int a) {
+        return (uint2*)(psm + NBUF * C::ROWBUF + a * C::META + C::IDS_BYTES);
     };
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -317,69 +338,62 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
     const uint64_t n_tiles = plan.totals[2], n_items = n_tiles + plan.totals[3];
     const bool use_table = plan.totals[5] != 0;
 
-    if (warp == CWARPS) {
+    if (warp >= CWARPS) {
+        const uint32_t pw = warp - CWARPS;  // producer index
+        uint64_t* p_st = p_st_all[pw];
+        uint32_t* p_off = p_off_all[pw];
         // ================================================= producer warp
         PROF_DECL
         unsigned long long item_next = 0;
         if (lane == 0) item_next = atomicAdd(work, 1ULL);
-        for (uint32_t k = 0;; ++k) {
-            const int b = k % NBUF;
+        // item -> descriptor area ma: member ids and chunk descriptors (blocking:
+        // bucket metadata and ids are two dependent round trips)
+        auto stage_meta = [&](int ma) {
             // the next grab is issued one item ahead so its latency overlaps this item
-            unsigned long long item = __shfl_sync(0xffffffffu, item_next, 0);
+            const unsigned long long item = __shfl_sync(0xffffffffu, item_next, 0);
             if (lane == 0 && item < n_items) item_next = atomicAdd(work, 1ULL);
-            PROF_START
-            if (k >= NBUF) mbar_wait(&empty_bar[b], ((k / NBUF) - 1) & 1);
-            PROF_STOP(0)
-            PROF_START
-            uint32_t* rows = rowsb(b);
-            uint32_t* ids = idsb(b);
-            uint2* chunks = chb(b);
+            uint32_t* ids = idsm(ma);
+            uint2* chunks = chm(ma);
             if (item >= n_items) {
-                if (lane == 0) s_nch[b] = NCH_DONE;
-                mbar_arrive_cp_async(&full_bar[b]);
-                mbar_arrive(&full_bar[b]);
-                break;
+                if (lane == 0) s_nch[ma] = NCH_DONE;
+                __syncwarp();
+                return;
             }
             if (lane == 0) {
-                s_nch[b] = 0;
-                s_next[b] = 0;
+                s_nch[ma] = 0;
+                s_next[ma] = 0;
             }
             __syncwarp();
             if (item < n_tiles) {
                 const uint64_t b0 = plan.tile_first[item], b1 = plan.tile_first[item + 1];
                 const uint32_t cnt = (uint32_t)(b1 - b0);
-                // the tile's bucket metadata -> shared memory in one async round trip
-                for (uint32_t i = lane; i <= cnt; i += 32) {
-                    cp_async8(m_mpre + i, plan.mpre + b0 + i);
-                    if (i < cnt) {
-                        cp_async4(m_bsize + i, bsize + b0 + i);
-                        cp_async8(m_bstart + i, bstart + b0 + i);
-                        cp_async4(m_btab + i, btab + b0 + i);
-                    }
-                }
-                cp_async_wait_all();
-                __syncwarp();
-                const uint64_t mbase = m_mpre[0];
-                // small buckets of the tile (order-preserving compaction, one lane per
-                // bucket) and their chunk descriptors
+                const uint64_t mbase = __ldg(plan.mpre + b0);
+                // small buckets of the tile (positive entries of the member prefix;
+                // big and left-out buckets count 0), order-preserving compaction with
+                // one lane per bucket, and their chunk descriptors
                 const uint32_t lt = (1u << lane) - 1u;
                 uint32_t nsb = 0;
                 for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
                     const uint32_t i = i0 + lane;
-                    const uint32_t s = i < cnt ? m_bsize[i] : 0u;
-                    const bool small = i < cnt && s <= L;
+                    uint64_t mp0 = 0, mp1 = 0;
+                    if (i < cnt) {
+                        mp0 = __ldg(plan.mpre + b0 + i);
+                        mp1 = __ldg(plan.mpre + b0 + i + 1);
+                    }
+                    const bool small = mp1 > mp0;
                     const uint32_t bal = __ballot_sync(0xffffffffu, small);
                     if (small) {
+                        const uint32_t s = (uint32_t)(mp1 - mp0);
                         const uint32_t kk = nsb + __popc(bal & lt);
-                        const uint32_t off = (uint32_t)(m_mpre[i] - mbase);
+                        const uint32_t off = (uint32_t)(mp0 - mbase);
                         p_off[kk] = off;
-                        p_st[kk] = m_bstart[i];
-                        const uint32_t cb = atomicAdd(&s_nch[b], count_chunks_tri(s));
-                        emit_chunks_tri(chunks, cb, off, s, m_btab[i]);
+                        p_st[kk] = __ldg(bstart + b0 + i);
+                        const uint32_t cb = atomicAdd(&s_nch[ma], count_chunks_tri(s));
+                        emit_chunks_tri(chunks, cb, off, s, __ldg(btab + b0 + i));
                     }
                     nsb += __popc(bal);
                 }
-                const uint32_t tot = (uint32_t)(m_mpre[cnt] - mbase);
+                const uint32_t tot = (uint32_t)(__ldg(plan.mpre + b1) - mbase);
                 if (lane == 0) p_off[nsb] = tot;
                 __syncwarp();
                 // member ids, one lane per member (bucket found by binary search)
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
                 }
                 cp_async_wait_all();
                 __syncwarp();
-                for (uint32_t r = lane; r < tot; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
+                if (lane == 0) s_nrows[ma] = tot;
             } else {
                 uint64_t bk;
                 uint32_t I, J;
@@ -443,15 +457,38 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
                             }
                         }
                     }
-                    s_nch[b] = cbase;
+                    s_nch[ma] = cbase;
                 }
                 cp_async_wait_all();
                 __syncwarp();
-                for (uint32_t r = lane; r < nI + nJ; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
+                if (lane == 0) s_nrows[ma] = nI + nJ;
+            }
+            __syncwarp();
+        };
+        stage_meta(pw % C::NMETA);
+        for (uint32_t k = pw;; k += NPROD) {
+            const int b = k % NBUF, ma = k % C::NMETA;
+            PROF_START
+            if (k >= NBUF) mbar_wait(&empty_bar[b], ((k / NBUF) - 1) & 1);
+            PROF_STOP(0)
+            PROF_START
+            if (s_nch[ma] == NCH_DONE) {
+                mbar_arrive_cp_async(&full_bar[b]);
+                mbar_arrive(&full_bar[b]);
+                break;
+            }
+            {
+                uint32_t* rows = rowsb(b);
+                const uint32_t* ids = idsm(ma);
+                const uint32_t nrows = s_nrows[ma];
+                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
             }
             __syncwarp();
             mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
-            mbar_arrive(&full_bar[b]);           // releases ids / descriptors / counters
+            mbar_arrive(&full_bar[b]);           // releases the descriptor of item k
+            // look ahead: the descriptor area of item k + NPROD belonged to item
+            // k + NPROD - NMETA = k - NBUF, released by the empty wait above
+            stage_meta((k + NPROD) % C::NMETA);
             PROF_STOP(1)
         }
         PROF_FLUSH(0)
@@ -460,7 +497,7 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
 
     // ===================================================== consumer warps
     PROF_DECL
-    uint32_t* qbase = (uint32_t*)(psm + NBUF * C::BUF) + warp * C::QWORDS;
+    uint32_t* qbase = (uint32_t*)(psm + NBUF * C::ROWBUF + C::NMETA * C::META) + warp * C::QWORDS;
     Queue q;
     q.qa = qbase;
     q.qb = q.qa + QCAP;
@@ -471,20 +508,26 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
     const uint32_t lt_mask = (1u << lane) - 1u;
     unsigned long long distinct = 0;
 
+    uint32_t finished = 0;  // bit p: producer p has no more items
     for (uint32_t k = 0;; ++k) {
-        const int bsel = k % NBUF;
+        const int bsel = k % NBUF, msel = k % C::NMETA;
+        if (finished & (1u << (k % NPROD))) continue;
         PROF_START
         mbar_wait(&full_bar[bsel], (k / NBUF) & 1);
         PROF_STOP(0)
         PROF_START
-        const uint32_t nch = s_nch[bsel];
-        if (nch == NCH_DONE) break;
+        const uint32_t nch = s_nch[msel];
+        if (nch == NCH_DONE) {
+            finished |= 1u << (k % NPROD);
+            if (finished == (1u << NPROD) - 1u) break;
+            continue;
+        }
         const uint32_t* rows = rowsb(bsel);
-        const uint32_t* ids = idsb(bsel);
-        const uint2* chunks = chb(bsel);
+        const uint32_t* ids = idsm(msel);
+        const uint2* chunks = chm(msel);
         while (true) {
             uint32_t ci = 0;
-            if (lane == 0) ci = atomicAdd(&s_next[bsel], 1u);
+            if (lane == 0) ci = atomicAdd(&s_next[msel], 1u);
             ci = __shfl_sync(0xffffffffu, ci, 0);
             if (ci >= nch) break;
             const uint2 d = chunks[ci];
@@ -518,8 +561,9 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
             }
             const uint32_t u_lo = tri ? apos + 1 : bbeg;  // pairs j > i within a bucket
             const bool excl_on = excl > 0;
-            const uint32_t* R = rows + bbeg * C::ROWP;
-            for (uint32_t u = bbeg; u < bend; ++u, R += C::ROWP) {
+            // evaluate the pair (a, row u): validity, tag-plane masks, queue decision
+            auto eval = [&](uint32_t u, const uint32_t* R, bool& slow, uint32_t& flags,
+                            uint32_t (&qmask)[W]) {
                 bool valid = a_ok && u >= u_lo;
                 if (excl_on || HAS_E) {
                     const uint32_t bid = ids[u];
@@ -528,20 +572,25 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
                         (p <= 1 || part_of(edges, p, bid) == a_part))
                         valid = false;
                 }
-                bool slow = false;
-                uint32_t qmask[W];
-                uint32_t flags = tflag;
+                slow = false;
+                flags = tflag;
                 // masks are computed for every lane (no divergence); invalid lanes drop them
                 if (MODE == MODE_MATCHED) {
+                    // the bucket's table T must be the pair's first collision, so a
+                    // pair with sim >= m collides in >= m - 1 tables after T: screen
+                    // on those words only (earlier words are built in push())
                     uint32_t cnt = 0;
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
-                        uint32_t s8 = pmask<W, NP>(A, R, w, 8);
-                        if (w == W - 1) s8 &= last_mask;
+                        uint32_t s8 = 0;
+                        if (w >= wt) {
+                            s8 = pmask<W, NP>(A, R, w, 8);
+                            if (w == W - 1) s8 &= last_mask;
+                            cnt += __popc(w == wt ? (s8 & ~((low << 1) | 1u)) : s8);
+                        }
                         qmask[w] = s8;
-                        cnt += __popc(s8);
                     }
-                    slow = valid && cnt >= m;
+                    slow = valid && cnt + 1 >= m;
                     flags |= QF_COUNT;
                 } else {
                     uint32_t early = 0, cnt = 0;
@@ -574,8 +623,17 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
                         }
                     }
                 }
+            };
+            // queue the warp's slow lanes; drain 32 once the queue holds 32
+            auto push = [&](uint32_t u, const uint32_t* R, bool slow, uint32_t flags,
+                            uint32_t (&qmask)[W]) {
                 const uint32_t bal = __ballot_sync(0xffffffffu, slow);
                 if (bal) {
+                    if (MODE == MODE_MATCHED) {
+#pragma unroll
+                        for (int w = 0; w < W; ++w)
+                            if (w < wt) qmask[w] = pmask<W, NP>(A, R, w, 8);
+                    }
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
                         q.qa[e] = a;
@@ -597,6 +655,25 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
                         qn -= 32;
                     }
                 }
+            };
+            uint32_t u = bbeg;
+            const uint32_t* R = rows + bbeg * C::ROWP;
+            if (MODE == MODE_MATCHED) {
+                // two B rows per step: independent LOP3 chains overlap their latencies
+                for (; u + 1 < bend; u += 2, R += 2 * C::ROWP) {
+                    bool s0, s1;
+                    uint32_t f0, f1, m0[W], m1[W];
+                    eval(u, R, s0, f0, m0);
+                    eval(u + 1, R + C::ROWP, s1, f1, m1);
+                    push(u, R, s0, f0, m0);
+                    push(u + 1, R + C::ROWP, s1, f1, m1);
+                }
+            }
+            for (; u < bend; ++u, R += C::ROWP) {
+                bool s0;
+                uint32_t f0, m0[W];
+                eval(u, R, s0, f0, m0);
+                push(u, R, s0, f0, m0);
             }
         }
         __syncwarp();
@@ -612,24 +689,28 @@ __global__ void __launch_bounds__(PTHREADS, QS_MINB) k_pairs_pc(
 }
 
 // --------------------------------------------------------------- planning
-__global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, uint64_t nb, uint32_t L,
+// buckets of tables > tmax are left out (MATCHED: a pair with sim >= m has its
+// first collision in a table <= t - m)
+__global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                             uint32_t tmax, uint64_t nb, uint32_t L,
                              uint64_t* __restrict__ small, uint64_t* __restrict__ bigflag) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = i < nb ? bsize[i] : 0;
+        const uint32_t s = (i < nb && btab[i] <= tmax) ? bsize[i] : 0;
         small[i] = (i < nb && s <= L) ? s : 0;
         bigflag[i] = (i < nb && s > L) ? 1 : 0;
     }
 }
 
 // per big bucket k: its item count (scan input) and bucket index
-__global__ void k_plan_big(const uint32_t* __restrict__ bsize, uint64_t nb, uint32_t L,
+__global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                           uint32_t tmax, uint64_t nb, uint32_t L,
                            const uint64_t* __restrict__ bigpos, uint64_t* __restrict__ bigb,
                            uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = bsize[i];
-        if (s <= L) continue;
+        if (s <= L || btab[i] > tmax) continue;
         const uint64_t k = bigpos[i];
         const uint64_t nseg = (s + L - 1) / L;
         bigb[k] = i;
@@ -665,11 +746,9 @@ __global__ void k_plan_tiles(const uint64_t* __restrict__ mpre, uint64_t nb, uin
     }
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k <= n_tiles;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        if (k == n_tiles) {
-            tile_first[k] = nb;
-            continue;
-        }
-        const uint64_t target = k * L;
+        // the last tile ends after the last small bucket (trailing big or
+        // left-out buckets belong to no tile)
+        const uint64_t target = k == n_tiles ? totals[0] : k * L;
         uint64_t lo = 0, hi = nb;
         while (lo < hi) {
             const uint64_t mid = (lo + hi) >> 1;
@@ -787,14 +866,15 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     unsigned long long* work = (unsigned long long*)(totals + 6);
     const uint64_t items_cap = (nb + 1) * 8;
     const unsigned g = qs_blocks(nb + 1, 256);
-    k_plan_sizes<<<g, 256, 0, st>>>(bsize, nb, L, mpre, bigpos);
+    const uint32_t tmax = MODE == MODE_MATCHED ? t - m : t - 1;
+    k_plan_sizes<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, mpre, bigpos);
     int rc = scan_u64(mpre, mpre, nb + 1, totals + 0, sws, st);
     if (rc) return rc;
     rc = scan_u64(bigpos, bigpos, nb + 1, totals + 1, sws, st);
     if (rc) return rc;
     QS_CUDA(cudaMemsetAsync(bigoff, 0, (nb + 1) * 8, st), "memset");
     QS_CUDA(cudaMemsetAsync(totals + 4, 0, 8, st), "memset");
-    k_plan_big<<<g, 256, 0, st>>>(bsize, nb, L, bigpos, bigb, bigoff,
+    k_plan_big<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, bigpos, bigb, bigoff,
                                   (unsigned long long*)(totals + 4));
     rc = scan_u64(bigoff, bigoff, nb + 1, nullptr, sws, st);
     if (rc) return rc;
@@ -811,7 +891,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     if (per_sm < 1) per_sm = 1;
     kern<<<num_sms() * per_sm, PTHREADS, C::SMEM, st>>>(sids, bstart, bsize, btab, plan, rkeys, tags,
                                                         n, t, m, excl, emask, edges, p, out_key,
-                                                        out_sim, cap, counters, work);
+                                                        out_sim, cap, counters, work, tmax);
     QS_CHECK_LAUNCH("k_pairs_pc");
     return QS_OK;
 }
