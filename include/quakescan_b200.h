@@ -136,13 +136,18 @@ int qs_lsh_bucket_stats(const uint32_t* sids_dev, const uint64_t* bstart_dev,
 /* Remove excluded members from every bucket (single partition only; an
  * excluded fingerprint can never be part of a counted pair there).  Writes
  * the compacted member ids and bucket list (buckets keeping >= 2 members);
- * counts_dev[0] = buckets kept, counts_dev[1] = members kept. */
+ * counts_dev[0] = buckets kept, counts_dev[1] = members kept.  When hist_dev
+ * is not NULL the same pass also produces the single-partition bucket
+ * statistics of qs_lsh_bucket_stats (hist/big/stats_out_dev as there,
+ * stats_out_dev zeroed by the caller). */
 size_t qs_lsh_compact_ws_bytes(uint64_t n_nonsingle);
 int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                            const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t nb,
                            const uint8_t* excluded_dev, uint32_t* sids2_dev,
                            uint64_t* bstart2_dev, uint32_t* bsize2_dev, uint32_t* btab2_dev,
-                           uint64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+                           uint64_t* counts_dev, uint64_t* hist_dev, uint32_t hist_len,
+                           uint32_t* big_dev, uint64_t big_cap, uint64_t* stats_out_dev,
+                           void* ws_dev, size_t ws_bytes, void* stream);
 
 /* Candidate-pair enumeration + exact collision counting + >= m threshold
  * (replaces _collect_pairs + the count filter, lsh_search.py:175-219, 261, 281).

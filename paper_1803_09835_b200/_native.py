@@ -45,7 +45,8 @@ SIGNATURES = {
     "qs_lsh_list_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "qs_lsh_bucket_stats": (_int, [_p, _p, _p, _u64, _p, _p, _u32, _p, _u32, _p, _u64, _p, _p]),
     "qs_lsh_compact_ws_bytes": (_sz, [_u64]),
-    "qs_lsh_compact_buckets": (_int, [_p, _p, _p, _p, _u64, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "qs_lsh_compact_buckets": (_int, [_p, _p, _p, _p, _u64, _p, _p, _p, _p, _p, _p,
+                                       _p, _u32, _p, _u64, _p, _p, _sz, _p]),
     "qs_lsh_pairs_ws_bytes": (_sz, [_u64]),
     "qs_lsh_pairs": (_int, [_p, _p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
                             _int, _p, _p, _u64, _p, _p, _sz, _p]),

@@ -228,30 +228,46 @@ __device__ __forceinline__ bool list_flag(const uint64_t* __restrict__ k, uint64
 
 constexpr int LIST_THREADS = 512;
 
+// per block: [0] heads of non-singleton buckets, [1] all heads
 __global__ void __launch_bounds__(LIST_THREADS) k_list_count(const uint64_t* __restrict__ k,
                                                              uint64_t n, uint64_t total,
-                                                             uint64_t chunk, int kind,
+                                                             uint64_t chunk, uint64_t nblk,
                                                              uint64_t* __restrict__ counts) {
-    __shared__ uint32_t red[LIST_THREADS / 32];
+    __shared__ uint32_t red[2][LIST_THREADS / 32];
     const uint64_t lo = blockIdx.x * chunk, hi = min(total, lo + chunk);
-    uint32_t c = 0;
-    for (uint64_t g = lo + threadIdx.x; g < hi; g += LIST_THREADS) c += list_flag(k, n, g, kind);
+    uint32_t c0 = 0, c1 = 0;
+    for (uint64_t g = lo + threadIdx.x; g < hi; g += LIST_THREADS) {
+        c0 += list_flag(k, n, g, 0);
+        c1 += list_flag(k, n, g, 2);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    for (int o = 16; o > 0; o >>= 1) {
+        c0 += __shfl_down_sync(0xffffffffu, c0, o);
+        c1 += __shfl_down_sync(0xffffffffu, c1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = c0;
+        red[1][threadIdx.x >> 5] = c1;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint64_t s = 0;
-        for (int w = 0; w < LIST_THREADS / 32; ++w) s += red[w];
-        counts[blockIdx.x] = s;
+        uint64_t s0 = 0, s1 = 0;
+        for (int w = 0; w < LIST_THREADS / 32; ++w) {
+            s0 += red[0][w];
+            s1 += red[1][w];
+        }
+        counts[blockIdx.x] = s0;
+        counts[nblk + blockIdx.x] = s1;
     }
 }
 
-// kind 0 writes global positions (uint64) of non-singleton heads; kind 1
-// writes in-table positions (uint32) of non-singleton tails.
+// One sweep writes both ends of every non-singleton bucket: heads store their
+// global position into bstart[i], tails their in-table position into bsize[i],
+// i = number of non-singleton heads at or before the element, minus one (the
+// head may sit in an earlier block: offs carries the count of earlier blocks).
 __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __restrict__ k,
                                                              uint64_t n, uint64_t total,
-                                                             uint64_t chunk, int kind,
+                                                             uint64_t chunk,
                                                              const uint64_t* __restrict__ offs,
                                                              uint64_t* __restrict__ out64,
                                                              uint32_t* __restrict__ out32) {
@@ -263,8 +279,16 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
     __syncthreads();
     for (uint64_t g0 = lo; g0 < hi; g0 += LIST_THREADS) {
         const uint64_t g = g0 + threadIdx.x;
-        const bool f = g < hi && list_flag(k, n, g, kind);
-        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        bool hd = false, tl = false;
+        if (g < hi) {
+            const uint64_t pos = g % n;
+            const uint64_t key = k[g];
+            const bool head = pos == 0 || k[g - 1] != key;
+            const bool tail = pos == n - 1 || k[g + 1] != key;
+            hd = head && !tail;
+            tl = tail && !head;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, hd);
         if (lane == 0) wsum[warp] = __popc(bal);
         __syncthreads();
         uint64_t wb = base;
@@ -273,11 +297,9 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
             if (w < (int)warp) wb += wsum[w];
             tot += wsum[w];
         }
-        if (f) {
-            const uint64_t o = wb + __popc(bal & ((1u << lane) - 1u));
-            if (kind == 0) out64[o] = g;
-            else out32[o] = (uint32_t)(g % n);
-        }
+        const uint64_t incl = wb + __popc(bal & (lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u)));
+        if (hd) out64[incl - 1] = g;
+        if (tl) out32[incl - 1] = (uint32_t)(g % n);
         __syncthreads();
         if (threadIdx.x == 0) base += tot;
         __syncthreads();
@@ -378,10 +400,21 @@ __global__ void __launch_bounds__(256) k_bucket_stats(
 // -------------------------------------------------- exclusion compaction
 // partitions == 1 only: an excluded member can never be part of a counted
 // pair, so it is removed from the bucket before enumeration.
-__global__ void k_keep_count(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
-                             const uint32_t* __restrict__ bsize, uint64_t nb,
-                             const uint8_t* __restrict__ ex, uint64_t* __restrict__ cnt,
-                             uint64_t* __restrict__ flag) {
+// keep counts per bucket; with `hist` (single partition) also the bucket
+// statistics of k_bucket_stats: one piece of size s per bucket, lookups
+// (s - 1)(s - e) with e excluded members (lsh_search.py:192-194)
+__global__ void __launch_bounds__(256) k_keep_count(
+    const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
+    const uint32_t* __restrict__ bsize, uint64_t nb, const uint8_t* __restrict__ ex,
+    uint64_t* __restrict__ cnt, uint64_t* __restrict__ flag, unsigned long long* __restrict__ hist,
+    uint32_t hist_len, uint32_t* __restrict__ big, uint64_t big_cap,
+    unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long sh[ST_HIST];
+    if (hist) {
+        for (int i = threadIdx.x; i < ST_HIST; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+    }
+    unsigned long long looks = 0, pieces = 0, mx = 0;
     for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
          b += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t st = bstart[b];
@@ -390,7 +423,28 @@ __global__ void k_keep_count(const uint32_t* __restrict__ sids, const uint64_t* 
         for (uint32_t j = 0; j < s; ++j) k += ex[sids[st + j]] == 0;
         cnt[b] = k >= 2 ? k : 0;
         flag[b] = k >= 2 ? 1 : 0;
+        if (hist) {
+            looks += (unsigned long long)(s - 1) * k;
+            ++pieces;
+            stats_piece(s, sh, hist, hist_len, big, big_cap, out, mx);
+        }
     }
+    if (!hist) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        looks += __shfl_down_sync(0xffffffffu, looks, o);
+        pieces += __shfl_down_sync(0xffffffffu, pieces, o);
+        unsigned long long y = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (looks) atomicAdd(out + 0, looks);
+        if (pieces) atomicAdd(out + 1, pieces);
+        if (mx) atomicMax(out + 3, mx);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ST_HIST; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
 __global__ void k_keep_write(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
@@ -570,7 +624,7 @@ static uint64_t list_blocks(uint64_t total) {
 
 size_t qs_lsh_list_ws_bytes(uint64_t n, uint32_t t) {
     uint64_t b = list_blocks(n * t);
-    return (size_t)(b + 1) * 8 + scan_ws_bytes(b) + 256;
+    return (size_t)(2 * b + 1) * 8 + scan_ws_bytes(b) + 256;
 }
 
 int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint64_t* bstart_dev,
@@ -585,26 +639,19 @@ int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t, uint6
     }
     const uint64_t B = list_blocks(total);
     const uint64_t chunk = (total + B - 1) / B;
-    uint64_t* cnt = (uint64_t*)ws_dev;
-    void* sws = (void*)(((uintptr_t)(cnt + B + 1) + 63) & ~(uintptr_t)63);
-    if (bstart_dev == nullptr) {
-        k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, 0, cnt);
-        int rc = scan_u64(cnt, cnt, B, counts_dev + 0, sws, st);
-        if (rc) return rc;
-        k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, 2, cnt);
-        rc = scan_u64(cnt, cnt, B, counts_dev + 1, sws, st);
-        if (rc) return rc;
-        QS_CHECK_LAUNCH("list count");
-        return QS_OK;
-    }
-    for (int kind = 0; kind < 2; ++kind) {
-        k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, kind, cnt);
-        int rc = scan_u64(cnt, cnt, B, kind == 0 ? counts_dev : nullptr, sws, st);
-        if (rc) return rc;
-        k_list_write<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, kind, cnt, bstart_dev,
+    uint64_t* cnt = (uint64_t*)ws_dev;  // [0, B): non-singleton heads, [B, 2B): all heads
+    void* sws = (void*)(((uintptr_t)(cnt + 2 * B + 1) + 63) & ~(uintptr_t)63);
+    k_list_count<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, B, cnt);
+    int rc = scan_u64(cnt, cnt, B, counts_dev + 0, sws, st);
+    if (rc) return rc;
+    rc = scan_u64(cnt + B, cnt + B, B, counts_dev + 1, sws, st);
+    if (rc) return rc;
+    if (bstart_dev != nullptr) {
+        k_list_write<<<B, LIST_THREADS, 0, st>>>(skeys_dev, n, total, chunk, cnt, bstart_dev,
                                                  bsize_dev);
+        k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev, btab_dev,
+                                              table_ids_dev);
     }
-    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart_dev, counts_dev, n, bsize_dev, btab_dev, table_ids_dev);
     QS_CHECK_LAUNCH("list buckets");
     return QS_OK;
 }
@@ -631,6 +678,8 @@ int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                            const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t nb,
                            const uint8_t* excluded_dev, uint32_t* sids2_dev, uint64_t* bstart2_dev,
                            uint32_t* bsize2_dev, uint32_t* btab2_dev, uint64_t* counts_dev,
+                           uint64_t* hist_dev, uint32_t hist_len, uint32_t* big_dev,
+                           uint64_t big_cap, uint64_t* stats_out_dev,
                            void* ws_dev, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     QS_ARG(ws_bytes >= qs_lsh_compact_ws_bytes(nb), "compact workspace too small");
@@ -643,7 +692,10 @@ int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
     uint64_t* slot = off + (nb + 1);
     void* sws = (void*)(((uintptr_t)(slot + nb + 1) + 63) & ~(uintptr_t)63);
     const unsigned g = qs_blocks(nb, 256);
-    k_keep_count<<<g, 256, 0, st>>>(sids_dev, bstart_dev, bsize_dev, nb, excluded_dev, cnt, slot);
+    if (hist_dev) QS_ARG(hist_len >= ST_HIST && stats_out_dev, "stats outputs: hist_len >= %d and out", ST_HIST);
+    k_keep_count<<<g, 256, 0, st>>>(sids_dev, bstart_dev, bsize_dev, nb, excluded_dev, cnt, slot,
+                                    (unsigned long long*)hist_dev, hist_len, big_dev, big_cap,
+                                    (unsigned long long*)stats_out_dev);
     int rc = scan_u64(cnt, off, nb, counts_dev + 1, sws, st);
     if (rc) return rc;
     rc = scan_u64(slot, slot, nb, counts_dev + 0, sws, st);

@@ -207,11 +207,13 @@ class DeviceSearch:
             nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, nat.ptr(self.bstart),
                      nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(self.table_ids),
                      nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
-        self.launches += 2 * 4 + 2 * 5 + 1
+        self.launches += 7 + 9
         self.full = (self.sids, self.bstart, self.bsize, self.btab, self.nb)
 
     def compact(self, emask):
-        """Bucket list with excluded members removed (partitions == 1)."""
+        """Bucket list with excluded members removed (partitions == 1).  The same
+        pass computes the single-partition bucket statistics for this emask
+        (returned later by bucket_stats)."""
         torch, lib = self.torch, nat.lib()
         self._mark("compact")
         nb = self.nb
@@ -220,13 +222,19 @@ class DeviceSearch:
         bsize2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         btab2 = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        hist = torch.zeros(_HIST_LEN, dtype=torch.int64, device=self.dev)
+        big_cap = max(1024, nb // 64)
+        big = torch.empty(big_cap, dtype=torch.int32, device=self.dev)
+        out = torch.zeros(4, dtype=torch.int64, device=self.dev)
         ws = self._empty(lib.qs_lsh_compact_ws_bytes(nb))
         nat.call("qs_lsh_compact_buckets", nat.ptr(self.sids), nat.ptr(self.bstart),
                  nat.ptr(self.bsize), nat.ptr(self.btab), nb, nat.ptr(emask), nat.ptr(sids2),
-                 nat.ptr(bstart2), nat.ptr(bsize2), nat.ptr(btab2), nat.ptr(counts), nat.ptr(ws),
+                 nat.ptr(bstart2), nat.ptr(bsize2), nat.ptr(btab2), nat.ptr(counts),
+                 nat.ptr(hist), _HIST_LEN, nat.ptr(big), big_cap, nat.ptr(out), nat.ptr(ws),
                  ws.numel(), nat.stream())
         self.launches += 2 + 2 * 3
         nb2 = int(counts[0].item())
+        self._compact_stats = (emask, hist, big, big_cap, out)
         return (sids2, bstart2, bsize2, btab2, nb2)
 
     def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None):
@@ -306,6 +314,13 @@ class DeviceSearch:
 
     def bucket_stats(self, emask, edges, p):
         torch = self.torch
+        cached = getattr(self, "_compact_stats", None)
+        if p == 1 and cached is not None and cached[0] is emask:
+            _, hist, big, big_cap, out = cached
+            looks, pieces, n_big, mx = (int(v) for v in out.tolist())
+            if n_big > big_cap:
+                raise RuntimeError("bucket size overflow list too small")
+            return looks, pieces, mx, hist.cpu().numpy(), big[:n_big].cpu().numpy()
         self._mark("stats")
         hist = torch.zeros(_HIST_LEN, dtype=torch.int64, device=self.dev)
         big_cap = max(1024, self.nb // 64)
