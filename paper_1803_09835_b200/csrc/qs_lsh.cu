@@ -170,20 +170,173 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
 // the thread at its start; if its full keys are not already grouped, the run
 // is insertion-sorted by full key (stable, so ids stay ascending per key).
 // Runs are short (mixed runs are rare prefix collisions), so cost ~ one pass.
+// Keys are sorted on their top (64 - SORT_LO) bits only; runs of equal prefix
+// holding several distinct keys (prefix collisions) are then restored to
+// full-key order.  Detection reads the sorted keys once, coalesced; only the
+// first out-of-order position of a run reports the run start.
+constexpr uint32_t SORT_LO = 40;
+
+constexpr uint32_t FIX_LMAX = 8192;   // elements sorted in shared memory per long run
+constexpr uint32_t FIX_LCAP = 65536;  // long runs listed per build
+
+__device__ void insertion_run(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, uint64_t g,
+                              uint64_t e) {
+    for (uint64_t i = g + 1; i < e; ++i) {
+        const uint64_t key = keys[i];
+        const uint32_t id = ids[i];
+        uint64_t j = i;
+        while (j > g && keys[j - 1] > key) {
+            keys[j] = keys[j - 1];
+            ids[j] = ids[j - 1];
+            --j;
+        }
+        keys[j] = key;
+        ids[j] = id;
+    }
+}
+
+__global__ void k_fix_detect(const uint64_t* __restrict__ keys, uint64_t n, uint64_t total,
+                             uint64_t* __restrict__ runs, uint64_t cap,
+                             unsigned long long* __restrict__ nruns) {
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pos = g % n;
+        if (pos == 0) continue;
+        const uint64_t k0 = keys[g], k1 = keys[g - 1];
+        if ((k0 >> SORT_LO) != (k1 >> SORT_LO) || k0 >= k1) continue;
+        // out of order at g: walk back to the run start; report only if no
+        // earlier out-of-order position in the run
+        uint64_t j = g - 1;
+        bool firstbad = true;
+        while (j > g - pos && (keys[j - 1] >> SORT_LO) == (k0 >> SORT_LO)) {
+            if (keys[j] < keys[j - 1]) firstbad = false;
+            --j;
+        }
+        if (!firstbad) continue;
+        const unsigned long long o = atomicAdd(nruns, 1ULL);
+        if (o < cap) runs[o] = j;
+    }
+}
+
+// each reported run restored to full-key order: one warp per run; runs of up
+// to 32 members are ranked in registers (key, then position: stable), longer
+// runs by one lane's insertion sort
+__global__ void k_fix_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids, uint64_t n,
+                           const uint64_t* __restrict__ runs, uint64_t cap,
+                           unsigned long long* __restrict__ nruns,
+                           ulonglong2* __restrict__ longruns) {
+    const uint64_t cnt = min((uint64_t)*nruns, cap);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; r < cnt; r += nw) {
+        const uint64_t g = runs[r];
+        const uint64_t seg_end = g - g % n + n;
+        const uint64_t pre = keys[g] >> SORT_LO;
+        // run length: 32-wide probes
+        uint64_t e = g;
+        while (true) {
+            const uint64_t i = e + lane;
+            const bool in = i < seg_end && (keys[i] >> SORT_LO) == pre;
+            const uint32_t bal = __ballot_sync(0xffffffffu, in);
+            if (bal != 0xffffffffu) {
+                e += __ffs(~bal) - 1;
+                break;
+            }
+            e += 32;
+        }
+        const uint64_t len = e - g;
+        if (len <= 32) {
+            const bool ok = lane < len;
+            const uint64_t k = ok ? keys[g + lane] : ~0ull;
+            const uint32_t id = ok ? ids[g + lane] : 0u;
+            uint32_t rank = 0;
+            for (uint32_t j = 0; j < len; ++j) {
+                const uint64_t kj = __shfl_sync(0xffffffffu, k, j);
+                rank += (kj < k) || (kj == k && j < lane);
+            }
+            __syncwarp();
+            if (ok) {
+                keys[g + rank] = k;
+                ids[g + rank] = id;
+            }
+        } else if (lane == 0) {
+            const unsigned long long o = atomicAdd(nruns + 1, 1ULL);
+            if (o < FIX_LCAP) longruns[o] = make_ulonglong2(g, len);
+            else insertion_run(keys, ids, g, e);  // overflow: serial (never seen at cfg1)
+        }
+        __syncwarp();
+    }
+}
+
+// runs longer than 32: one CTA per run, stable bitonic sort of (key, position)
+// in shared memory (FIX_LMAX elements); longer runs by serial insertion
+__global__ void __launch_bounds__(1024) k_fix_long_runs(uint64_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ ids,
+                                                        const ulonglong2* __restrict__ longruns,
+                                                        const unsigned long long* __restrict__ nruns) {
+    extern __shared__ __align__(16) unsigned char fx_smem[];
+    uint64_t* sk = (uint64_t*)fx_smem;                 // [FIX_LMAX]
+    uint32_t* sp = (uint32_t*)(sk + FIX_LMAX);         // [FIX_LMAX] original position
+    uint32_t* si = sp + FIX_LMAX;                      // [FIX_LMAX] ids in original order
+    const uint64_t cnt = min((uint64_t)nruns[1], (uint64_t)FIX_LCAP);
+    for (uint64_t r = blockIdx.x; r < cnt; r += gridDim.x) {
+        const uint64_t g = longruns[r].x, len = longruns[r].y;
+        if (len > FIX_LMAX) {
+            if (threadIdx.x == 0) insertion_run(keys, ids, g, g + len);
+            __syncthreads();
+            continue;
+        }
+        uint32_t P = 1;
+        while (P < len) P <<= 1;
+        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+            sk[i] = i < len ? keys[g + i] : ~0ull;
+            sp[i] = i;
+            if (i < len) si[i] = ids[g + i];
+        }
+        __syncthreads();
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                    const uint32_t l = i ^ j;
+                    if (l > i) {
+                        const bool up = (i & k) == 0;
+                        const uint64_t a = sk[i], b = sk[l];
+                        const uint32_t pa = sp[i], pb = sp[l];
+                        const bool gt = a > b || (a == b && pa > pb);
+                        if (gt == up) {
+                            sk[i] = b; sk[l] = a;
+                            sp[i] = pb; sp[l] = pa;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+            keys[g + i] = sk[i];
+            ids[g + i] = si[sp[i]];
+        }
+        __syncthreads();
+    }
+}
+
+// fallback when the run list overflowed: every run start fixes its own run
 __global__ void k_fix_prefix_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
-                                  uint64_t n, uint64_t total) {
+                                  uint64_t n, uint64_t total, uint64_t cap,
+                                  const unsigned long long* __restrict__ nruns) {
+    if (*nruns <= cap) return;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
          g += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t pos = g % n;
         const uint64_t k0 = keys[g];
-        if (pos != 0 && (keys[g - 1] >> 32) == (k0 >> 32)) continue;  // not a run start
+        if (pos != 0 && (keys[g - 1] >> SORT_LO) == (k0 >> SORT_LO)) continue;  // not a run start
         const uint64_t seg_end = g - pos + n;
         uint64_t e = g + 1;
         bool sorted = true;
         uint64_t prev = k0;
         while (e < seg_end) {
             const uint64_t k = keys[e];
-            if ((k >> 32) != (k0 >> 32)) break;
+            if ((k >> SORT_LO) != (k0 >> SORT_LO)) break;
             if (k < prev) sorted = false;
             prev = k;
             ++e;
@@ -271,25 +424,47 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
                                                              const uint64_t* __restrict__ offs,
                                                              uint64_t* __restrict__ out64,
                                                              uint32_t* __restrict__ out32) {
+    constexpr int PER = 4;  // consecutive elements per thread
     __shared__ uint32_t wsum[LIST_THREADS / 32];
     __shared__ uint64_t base;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t lo = blockIdx.x * chunk, hi = min(total, lo + chunk);
     if (threadIdx.x == 0) base = offs[blockIdx.x];
     __syncthreads();
-    for (uint64_t g0 = lo; g0 < hi; g0 += LIST_THREADS) {
-        const uint64_t g = g0 + threadIdx.x;
-        bool hd = false, tl = false;
-        if (g < hi) {
-            const uint64_t pos = g % n;
-            const uint64_t key = k[g];
-            const bool head = pos == 0 || k[g - 1] != key;
-            const bool tail = pos == n - 1 || k[g + 1] != key;
-            hd = head && !tail;
-            tl = tail && !head;
+    for (uint64_t g0 = lo; g0 < hi; g0 += LIST_THREADS * PER) {
+        const uint64_t gt = g0 + (uint64_t)threadIdx.x * PER;
+        bool hd[PER], tl[PER];
+        uint32_t c = 0;
+        if (gt < hi) {
+            uint64_t kk[PER + 2];
+#pragma unroll
+            for (int e = 0; e < PER + 2; ++e) {
+                const uint64_t i = gt + e - 1;
+                kk[e] = (i < total && (e > 0 || gt > 0)) ? k[i] : 0;
+            }
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const uint64_t g = gt + e;
+                const uint64_t pos = g % n;
+                const bool in = g < hi;
+                const bool head = pos == 0 || kk[e] != kk[e + 1];
+                const bool tail = pos == n - 1 || kk[e + 2] != kk[e + 1];
+                hd[e] = in && head && !tail;
+                tl[e] = in && tail && !head;
+                c += hd[e];
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < PER; ++e) hd[e] = tl[e] = false;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, hd);
-        if (lane == 0) wsum[warp] = __popc(bal);
+        // block exclusive scan of per-thread head counts
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
         __syncthreads();
         uint64_t wb = base;
         uint32_t tot = 0;
@@ -297,9 +472,13 @@ __global__ void __launch_bounds__(LIST_THREADS) k_list_write(const uint64_t* __r
             if (w < (int)warp) wb += wsum[w];
             tot += wsum[w];
         }
-        const uint64_t incl = wb + __popc(bal & (lane == 31 ? 0xFFFFFFFFu : ((2u << lane) - 1u)));
-        if (hd) out64[incl - 1] = g;
-        if (tl) out32[incl - 1] = (uint32_t)(g % n);
+        uint64_t incl = wb + x - c;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            incl += hd[e];
+            if (hd[e]) out64[incl - 1] = gt + e;
+            if (tl[e]) out32[incl - 1] = (uint32_t)((gt + e) % n);
+        }
         __syncthreads();
         if (threadIdx.x == 0) base += tot;
         __syncthreads();
@@ -580,8 +759,13 @@ int qs_lsh_prep(const uint64_t* sigs_dev, uint64_t n, uint32_t t, uint64_t* keys
     return QS_OK;
 }
 
+// reported-run capacity of the prefix fix-up (overflow falls back to a full scan)
+static uint64_t fix_cap(uint64_t total) { return total / 16 + 1024; }
+
 size_t qs_lsh_bucket_ws_bytes(uint64_t n, uint32_t t) {
-    return (size_t)n * t * (sizeof(uint64_t) + sizeof(uint32_t)) + radix_ws_bytes(n, t) + 512;
+    const uint64_t total = n * t;
+    return (size_t)total * (sizeof(uint64_t) + sizeof(uint32_t)) + radix_ws_bytes(n, t) +
+           fix_cap(total) * 8 + (size_t)FIX_LCAP * 16 + 1024;
 }
 
 int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t, uint64_t* keys_out_dev,
@@ -594,24 +778,31 @@ int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t, uint6
     unsigned char* w = (unsigned char*)ws_dev;
     uint64_t* alt_k = (uint64_t*)w;
     uint32_t* alt_v = (uint32_t*)(w + total * 8);
-    void* rws = (void*)(((uintptr_t)(w + total * 12) + 255) & ~(uintptr_t)255);
-    if (keys_out_dev != keys_dev)
-        QS_CUDA(cudaMemcpyAsync(keys_out_dev, keys_dev, total * 8, cudaMemcpyDeviceToDevice, st), "copy keys");
-    k_iota_segments<<<qs_blocks(total, 256), 256, 0, st>>>(ids_out_dev, n, t);
-    QS_CHECK_LAUNCH("k_iota_segments");
-    int in_alt = 0;
-    // keys are fmix64-mixed, so their top 32 bits already separate almost every
-    // pair of distinct keys: sort on bits [32, 64) only (4 passes instead of 8),
-    // then restore full-key order inside the rare runs whose prefixes collide.
-    int rc = radix_sort_pairs(keys_out_dev, ids_out_dev, n, t, 64, alt_k, alt_v, rws,
-                              radix_ws_bytes(n, t), &in_alt, st, 32);
+    unsigned char* rest = (unsigned char*)(((uintptr_t)(w + total * 12) + 255) & ~(uintptr_t)255);
+    void* rws = rest;
+    const size_t rws_bytes = radix_ws_bytes(n, t);
+    unsigned long long* nruns =
+        (unsigned long long*)(((uintptr_t)(rest + rws_bytes) + 255) & ~(uintptr_t)255);
+    ulonglong2* longruns = (ulonglong2*)(nruns + 32);
+    uint64_t* runs = (uint64_t*)(longruns + FIX_LCAP);
+    const uint64_t cap = fix_cap(total);
+    // keys are fmix64-mixed, so their top 24 bits separate almost all distinct
+    // keys: sort (stably, ids = in-table position) on bits [40, 64) in three
+    // 8-bit passes straight from the caller's keys, then restore full-key order
+    // in the runs whose prefixes collide
+    int rc = radix_sort_pairs_to(keys_dev, nullptr, n, t, SORT_LO, 64, keys_out_dev, ids_out_dev,
+                                 alt_k, alt_v, rws, rws_bytes, st);
     if (rc) return rc;
-    if (in_alt) {
-        QS_CUDA(cudaMemcpyAsync(keys_out_dev, alt_k, total * 8, cudaMemcpyDeviceToDevice, st), "copy");
-        QS_CUDA(cudaMemcpyAsync(ids_out_dev, alt_v, total * 4, cudaMemcpyDeviceToDevice, st), "copy");
-    }
-    k_fix_prefix_runs<<<qs_blocks(total, 256), 256, 0, st>>>(keys_out_dev, ids_out_dev, n, total);
-    QS_CHECK_LAUNCH("k_fix_prefix_runs");
+    QS_CUDA(cudaMemsetAsync(nruns, 0, 16, st), "memset");
+    const unsigned g = qs_blocks(total, 256);
+    k_fix_detect<<<g, 256, 0, st>>>(keys_out_dev, n, total, runs, cap, nruns);
+    k_fix_runs<<<148 * 16, 256, 0, st>>>(keys_out_dev, ids_out_dev, n, runs, cap, nruns, longruns);
+    const int long_smem = (int)(FIX_LMAX * 16);
+    QS_CUDA(cudaFuncSetAttribute(k_fix_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 long_smem), "smem attr");
+    k_fix_long_runs<<<148, 1024, long_smem, st>>>(keys_out_dev, ids_out_dev, longruns, nruns);
+    k_fix_prefix_runs<<<g, 256, 0, st>>>(keys_out_dev, ids_out_dev, n, total, cap, nruns);
+    QS_CHECK_LAUNCH("fix prefix runs");
     return QS_OK;
 }
 

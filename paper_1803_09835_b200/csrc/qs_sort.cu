@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         const uint64_t i = t0 + (uint64_t)r * 32 + lane;
         const bool ok = i < seg_len;
         k[r] = ok ? keys[base + i] : 0;
-        v[r] = ok ? vals[base + i] : 0;
+        v[r] = ok ? (vals ? vals[base + i] : (uint32_t)i) : 0;  // no vals: in-segment position
         const uint32_t dgt = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : 0x100u;
         const uint32_t peers = __match_any_sync(0xffffffffu, dgt);
         const uint32_t cnt = __popc(peers);
@@ -210,6 +210,42 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t 
         uint64_t* tk = src_k; src_k = dst_k; dst_k = tk;
         uint32_t* tv = src_v; src_v = dst_v; dst_v = tv;
         *in_alt ^= 1;
+    }
+    return QS_OK;
+}
+
+// Same sort with separate input / output buffers: the first pass reads
+// keys_in (left untouched) and vals_in (NULL: each value is its in-segment
+// position), passes alternate between out and alt so the last lands in out.
+int radix_sort_pairs_to(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t seg_len,
+                        uint32_t segments, uint32_t bit_lo, uint32_t key_bits, uint64_t* keys_out,
+                        uint32_t* vals_out, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+    if (seg_len == 0 || segments == 0) return QS_OK;
+    QS_ARG(seg_len < (1ull << 32), "radix sort segment longer than 2^32");
+    QS_ARG(ws_bytes >= radix_ws_bytes(seg_len, segments), "radix sort workspace too small");
+    QS_ARG(key_bits > bit_lo && (key_bits - bit_lo) % 8 == 0, "whole 8-bit digits only");
+    const uint32_t tiles = rs_tiles(seg_len);
+    QS_ARG(tiles <= 65535u * 64u, "too many tiles");
+    uint32_t* hist = (uint32_t*)ws;
+    QS_CUDA(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 RS_TILE * 12), "smem attr");
+    const uint32_t passes = (key_bits - bit_lo) / 8;
+    const uint64_t* src_k = keys_in;
+    const uint32_t* src_v = vals_in;
+    for (uint32_t ps = 0; ps < passes; ++ps) {
+        const uint32_t shift = bit_lo + 8 * ps;
+        const bool to_out = ((passes - 1 - ps) & 1) == 0;
+        uint64_t* dst_k = to_out ? keys_out : keys_alt;
+        uint32_t* dst_v = to_out ? vals_out : vals_alt;
+        dim3 grid(tiles, segments);
+        k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
+        k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
+        k_rs_scatter<<<grid, RS_THREADS, RS_TILE * 12, st>>>(src_k, src_v, seg_len, tiles, shift,
+                                                             hist, dst_k, dst_v);
+        QS_CHECK_LAUNCH("radix sort pass");
+        src_k = dst_k;
+        src_v = dst_v;
     }
     return QS_OK;
 }

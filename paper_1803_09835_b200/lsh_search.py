@@ -192,7 +192,7 @@ class DeviceSearch:
         nat.call("qs_lsh_build_buckets", nat.ptr(self.keys), n, t, nat.ptr(skeys),
                  nat.ptr(self.sids), nat.ptr(ws), ws.numel(), nat.stream())
         del ws
-        self.launches += 2 + 3 * 8
+        self.launches += 3 * 3 + 3
         self._mark("list")
         lws = self._empty(lib.qs_lsh_list_ws_bytes(n, t))
         counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
