@@ -9,7 +9,10 @@
 
 namespace qs {
 
-constexpr int RS_THREADS = 256;
+#ifndef QS_RS_THREADS
+#define QS_RS_THREADS 256
+#endif
+constexpr int RS_THREADS = QS_RS_THREADS;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per tile
 constexpr int RS_WARPS = RS_THREADS / 32;
