@@ -259,6 +259,15 @@ int qs_fp_haar2d(double* data_dev, uint64_t B, uint32_t H, uint32_t W, const int
 int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const double* med_dev,
                     const double* mad_dev, double* out_dev, void* stream);
 
+/* .fp file records (fingerprint.py:529-551 layout: index u64 | epoch f64 |
+ * bits u32[K], little endian, 16 + 4K bytes each) packed from / unpacked to
+ * device columns, so fingerprint files stream through one D2H / H2D copy. */
+int qs_fp_pack_records(const uint64_t* indices_dev, const double* epochs_dev,
+                       const uint32_t* bits_dev, uint64_t n, uint32_t K, uint8_t* out_dev,
+                       void* stream);
+int qs_fp_unpack_records(const uint8_t* in_dev, uint64_t n, uint32_t K, uint64_t* indices_dev,
+                         double* epochs_dev, uint32_t* bits_dev, void* stream);
+
 /* Generic stable LSD radix sort of (uint64 key, uint32 value) pairs over
  * `segments` independent equal-length segments, on key bits [0, key_bits). */
 size_t qs_radix_sort_ws_bytes(uint64_t seg_len, uint32_t segments);

@@ -474,6 +474,40 @@ __global__ void __launch_bounds__(WIN_THREADS) k_haar_batch(double* __restrict__
 
 using namespace qs;
 
+// ------------------------------------------------------ .fp record packing
+// record r (16 + 4K bytes, fingerprint.py:549-551): index u64 | epoch f64 |
+// bits u32[K], little endian; one thread per 32-bit output word (coalesced).
+__global__ void k_fp_pack(const uint64_t* __restrict__ idx, const double* __restrict__ ep,
+                          const uint32_t* __restrict__ bits, uint64_t n, uint32_t K,
+                          uint32_t* __restrict__ out) {
+    const uint64_t words = n * (4ull + K);
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = w / (4ull + K);
+        const uint32_t c = (uint32_t)(w - r * (4ull + K));
+        uint32_t v;
+        if (c < 2) v = (uint32_t)(idx[r] >> (32 * c));
+        else if (c < 4) v = (uint32_t)(__double_as_longlong(ep[r]) >> (32 * (c - 2)));
+        else v = bits[r * K + (c - 4)];
+        out[w] = v;
+    }
+}
+
+__global__ void k_fp_unpack(const uint32_t* __restrict__ in, uint64_t n, uint32_t K,
+                            uint64_t* __restrict__ idx, double* __restrict__ ep,
+                            uint32_t* __restrict__ bits) {
+    const uint64_t words = n * (4ull + K);
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = w / (4ull + K);
+        const uint32_t c = (uint32_t)(w - r * (4ull + K));
+        if (c == 0) idx[r] = (uint64_t)in[w] | ((uint64_t)in[w + 1] << 32);
+        else if (c == 2)
+            ep[r] = __longlong_as_double((long long)((uint64_t)in[w] | ((uint64_t)in[w + 1] << 32)));
+        else if (c >= 4) bits[r * K + (c - 4)] = in[w];
+    }
+}
+
 extern "C" {
 
 int qs_fp_band_stft(const void* x_dev, int x_is_f32, uint64_t n_samples, uint32_t frame,
@@ -593,6 +627,27 @@ int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const doubl
     k_normalize<<<qs_blocks(B * n, 256), 256, 0, (cudaStream_t)stream>>>(coeffs_dev, B * n, n, med_dev,
                                                                          mad_dev, out_dev);
     QS_CHECK_LAUNCH("k_normalize");
+    return QS_OK;
+}
+
+int qs_fp_pack_records(const uint64_t* indices_dev, const double* epochs_dev,
+                       const uint32_t* bits_dev, uint64_t n, uint32_t K, uint8_t* out_dev,
+                       void* stream) {
+    QS_ARG(K >= 1, "top_k must be >= 1");
+    if (n == 0) return QS_OK;
+    k_fp_pack<<<qs_blocks(n * (4ull + K), 256), 256, 0, (cudaStream_t)stream>>>(
+        indices_dev, epochs_dev, bits_dev, n, K, (uint32_t*)out_dev);
+    QS_CHECK_LAUNCH("k_fp_pack");
+    return QS_OK;
+}
+
+int qs_fp_unpack_records(const uint8_t* in_dev, uint64_t n, uint32_t K, uint64_t* indices_dev,
+                         double* epochs_dev, uint32_t* bits_dev, void* stream) {
+    QS_ARG(K >= 1, "top_k must be >= 1");
+    if (n == 0) return QS_OK;
+    k_fp_unpack<<<qs_blocks(n * (4ull + K), 256), 256, 0, (cudaStream_t)stream>>>(
+        (const uint32_t*)in_dev, n, K, indices_dev, epochs_dev, bits_dev);
+    QS_CHECK_LAUNCH("k_fp_unpack");
     return QS_OK;
 }
 

@@ -220,6 +220,13 @@ def _csr(mat: np.ndarray):
     return np.cumsum(off).astype(np.int32), cols.astype(np.int32), mat[rows, cols].astype(np.float64)
 
 
+def _to_host_pinned(t) -> np.ndarray:
+    """D2H into pinned host memory (the returned array keeps it alive)."""
+    buf = nat.torch().empty(t.shape, dtype=t.dtype, pin_memory=True)
+    buf.copy_(t)
+    return buf.numpy()
+
+
 class _Chain:
     """Device state of one channel: samples, band spectrogram and the
     window-kernel tables (geometry of fingerprint.py:198-243)."""
@@ -243,10 +250,8 @@ class _Chain:
             if xd.dtype not in (torch.float32, torch.float64):
                 xd = xd.to(torch.float64)
         else:
-            xh = np.ascontiguousarray(x, dtype=np.float64)
-            # float32-representable traces travel as float32 (exact widening on the device)
-            x32 = xh.astype(np.float32)
-            xd = torch.from_numpy(x32 if np.array_equal(x32.astype(np.float64), xh) else xh).cuda()
+            from .lsh_search import _to_device_staged
+            xd = _to_device_staged(np.ascontiguousarray(x, dtype=np.float64))
         self.x = xd
         taper = np.hanning(self.frame)
         j = np.arange(self.frame)
@@ -494,7 +499,7 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
     ch.check_finite()
     indices = np.arange(total, dtype=np.uint64)
     epochs = ts.start_epoch_s + np.arange(total) * params.window_lag_s
-    out_bits = bits if nat.is_device_tensor(ts.samples) else bits.cpu().numpy().view(np.uint32)
+    out_bits = bits if nat.is_device_tensor(ts.samples) else _to_host_pinned(bits).view(np.uint32)
     fps = FingerprintSet(d=params.d, top_k=params.top_k, window_len_s=params.window_len_s,
                          window_lag_s=params.window_lag_s, indices=indices, epochs=epochs,
                          bits=out_bits,
@@ -502,3 +507,139 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
                                "sample_rate_hz": ts.sample_rate_hz,
                                "start_epoch_s": ts.start_epoch_s})
     return fps, stats
+
+
+# ---------------------------------------------------------------------------
+# fingerprint and MAD files (fingerprint.py:392-417, 529-578)
+
+import os  # noqa: E402
+
+from . import container as _container  # noqa: E402
+from . import hostio  # noqa: E402
+from .errors import ConsistencyError as _ConsistencyError  # noqa: E402
+
+FP_MAGIC = b"QSFP0001"
+MAD_MAGIC = b"QSMD0001"
+_FP_KIND = "fingerprint"
+_MAD_KIND = "mad-stats"
+_FP_KEYS = ("d", "top_k", "window_len_s", "window_lag_s")
+
+
+def _fp_record_dtype(top_k: int):
+    return np.dtype([("index", "<u8"), ("epoch", "<f8"), ("bits", "<u4", (top_k,))])
+
+
+def _validate_device(fps) -> None:
+    torch = nat.torch()
+    n = len(fps)
+    b = fps.bits
+    if tuple(b.shape) != (n, fps.top_k) or fps.epochs.shape != (n,):
+        raise CorruptInputError("fingerprint arrays are inconsistent")
+    if n == 0:
+        return
+    if int(b.max().item()) >= fps.d or int(b.min().item()) < 0:
+        raise CorruptInputError("fingerprint bit index out of range")
+    if fps.top_k > 1 and not bool(torch.all((b[:, 1:] >> 1) - (b[:, :-1] >> 1) >= 1).item()):
+        raise CorruptInputError(
+            "fingerprint bits must be ascending with one sign bit per coefficient")
+
+
+def write_fingerprint_file(path, fps: FingerprintSet, extra: dict | None = None) -> None:
+    """Binary .fp file (fingerprint.py:529-551), byte-identical to the reference's.
+    CUDA bits are packed into records on the device and streamed to the file."""
+    device = nat.is_device_tensor(fps.bits)
+    if device:
+        _validate_device(fps)
+    else:
+        fps.validate()
+    header = {"d": fps.d, "top_k": fps.top_k, "window_len_s": fps.window_len_s,
+              "window_lag_s": fps.window_lag_s}
+    header.update(fps.meta)
+    if extra:
+        header.update(extra)
+    n = len(fps)
+    with open(path, "wb") as f:
+        _container.write_preamble(f, FP_MAGIC, header, count=n)
+        if not device:
+            rec = np.zeros(n, dtype=_fp_record_dtype(fps.top_k))
+            rec["index"] = fps.indices
+            rec["epoch"] = fps.epochs
+            rec["bits"] = fps.bits
+            rec.tofile(f)
+            return
+        torch = nat.torch()
+        dev = fps.bits.device
+        idx = torch.from_numpy(np.ascontiguousarray(fps.indices, dtype=np.uint64).view(np.int64)).to(dev)
+        ep = torch.from_numpy(np.ascontiguousarray(fps.epochs, dtype=np.float64)).to(dev)
+        bits = fps.bits.contiguous()
+        out = torch.empty(n * (16 + 4 * fps.top_k), dtype=torch.uint8, device=dev)
+        nat.call("qs_fp_pack_records", nat.ptr(idx), nat.ptr(ep), nat.ptr(bits), n, fps.top_k,
+                 nat.ptr(out), nat.stream())
+        hostio.write_device_bytes(f, out)
+
+
+def read_fingerprint_file(path, device: bool = False) -> FingerprintSet:
+    """Read a .fp file (fingerprint.py:554-578).  device=True returns CUDA
+    bits (int32), unpacked from the records on the GPU."""
+    with open(path, "rb") as f:
+        header, count, off = _container.read_preamble(f, FP_MAGIC, _FP_KIND)
+        for key in _FP_KEYS:
+            if key not in header:
+                raise _ConsistencyError(f"fingerprint header missing '{key}'")
+        top_k = int(header["top_k"])
+        dtype = _fp_record_dtype(top_k)
+        size = os.fstat(f.fileno()).st_size
+        _container.check_payload_size(size, off, count, dtype.itemsize, _FP_KIND)
+        if device:
+            torch = nat.torch()
+            raw = hostio.read_to_device(f, count * dtype.itemsize)
+            idx = torch.empty(count, dtype=torch.int64, device="cuda")
+            ep = torch.empty(count, dtype=torch.float64, device="cuda")
+            bits = torch.empty((count, top_k), dtype=torch.int32, device="cuda")
+            nat.call("qs_fp_unpack_records", nat.ptr(raw), count, top_k, nat.ptr(idx),
+                     nat.ptr(ep), nat.ptr(bits), nat.stream())
+            del raw
+            indices = idx.cpu().numpy().view(np.uint64)
+            epochs = ep.cpu().numpy()
+        else:
+            rec = np.fromfile(f, dtype=dtype, count=count)
+            indices = rec["index"].astype(np.uint64)
+            epochs = rec["epoch"].astype(np.float64)
+            bits = np.ascontiguousarray(rec["bits"])
+    meta = {k: v for k, v in header.items() if k not in _FP_KEYS}
+    fps = FingerprintSet(d=int(header["d"]), top_k=top_k,
+                         window_len_s=float(header["window_len_s"]),
+                         window_lag_s=float(header["window_lag_s"]),
+                         indices=indices, epochs=epochs, bits=bits, meta=meta)
+    if device:
+        _validate_device(fps)
+    else:
+        fps.validate()
+    return fps
+
+
+def write_mad_file(path, stats: MadStats, extra: dict | None = None) -> None:
+    """Binary MAD statistics (fingerprint.py:392-404): f64 medians then f64 MADs."""
+    header = {"rate": stats.rate, "seed": stats.seed, "n_sampled": stats.n_sampled,
+              "n_total": stats.n_total}
+    if extra:
+        header.update(extra)
+    with open(path, "wb") as f:
+        _container.write_preamble(f, MAD_MAGIC, header, count=stats.n_coeffs)
+        f.write(np.asarray(stats.median).astype("<f8").tobytes())
+        f.write(np.asarray(stats.mad).astype("<f8").tobytes())
+
+
+def read_mad_file(path):
+    """-> (MadStats, header) (fingerprint.py:407-417)."""
+    with open(path, "rb") as f:
+        header, count, off = _container.read_preamble(f, MAD_MAGIC, _MAD_KIND)
+        size = os.fstat(f.fileno()).st_size
+        _container.check_payload_size(size, off, count, 16, _MAD_KIND)
+        median = np.fromfile(f, dtype="<f8", count=count)
+        mad = np.fromfile(f, dtype="<f8", count=count)
+    stats = MadStats(median=median, mad=mad, rate=float(header.get("rate", 1.0)),
+                     seed=int(header.get("seed", 0)),
+                     n_sampled=int(header.get("n_sampled", count)),
+                     n_total=int(header.get("n_total", count)))
+    return stats, header

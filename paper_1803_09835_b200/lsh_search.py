@@ -585,3 +585,109 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
     if on_device:
         return trip, stats, mapping
     return trip.cpu().numpy().view(TRIPLET_DTYPE), stats, mapping
+
+
+# ---------------------------------------------------------------------------
+# triplet files (lsh_search.py:336-416)
+
+from . import container as _container  # noqa: E402
+from . import hostio  # noqa: E402
+from .errors import CorruptInputError  # noqa: E402
+
+TRI_MAGIC = b"QSTR0001"
+_TRI_KIND = "triplet"
+
+
+def write_triplet_file(path, triplets, header: dict) -> None:
+    """Binary triplet file, records sorted by (dt, idx1) as given.  Accepts the
+    host record array or the packed CUDA uint8 tensor a device search returns
+    (streamed to the file through pinned buffers)."""
+    if nat.is_device_tensor(triplets):
+        if triplets.numel() % TRIPLET_DTYPE.itemsize:
+            raise ParameterError("device triplets must be packed 20-byte records")
+        count = triplets.numel() // TRIPLET_DTYPE.itemsize
+        with open(path, "wb") as f:
+            _container.write_preamble(f, TRI_MAGIC, header, count=count)
+            hostio.write_device_bytes(f, triplets)
+        return
+    triplets = np.asarray(triplets, dtype=TRIPLET_DTYPE)
+    with open(path, "wb") as f:
+        _container.write_preamble(f, TRI_MAGIC, header, count=triplets.size)
+        triplets.tofile(f)
+
+
+def read_triplet_file(path, device: bool = False):
+    """-> (records, header); device=True returns the packed CUDA uint8 tensor."""
+    with open(path, "rb") as f:
+        header, count, off = _container.read_preamble(f, TRI_MAGIC, _TRI_KIND)
+        size = os.fstat(f.fileno()).st_size
+        _container.check_payload_size(size, off, count, TRIPLET_DTYPE.itemsize, _TRI_KIND)
+        if device:
+            rec = hostio.read_to_device(f, count * TRIPLET_DTYPE.itemsize)
+            if count:
+                torch = nat.torch()
+                dt = rec.view(count, TRIPLET_DTYPE.itemsize)[:, :8].contiguous().view(torch.int64)
+                if int(dt.min().item()) < 1:
+                    raise CorruptInputError("triplet with non-positive dt")
+            return rec, header
+        rec = np.fromfile(f, dtype=TRIPLET_DTYPE, count=count)
+    if rec.size and int(rec["dt"].min()) < 1:
+        raise CorruptInputError("triplet with non-positive dt")
+    return rec, header
+
+
+def iter_triplet_batches(path, start: int = 0, stop: int | None = None, batch: int = 1 << 16):
+    """Yield record batches of rows [start, stop) (lsh_search.py:360-377)."""
+    with open(path, "rb") as f:
+        _, count, off = _container.read_preamble(f, TRI_MAGIC, _TRI_KIND)
+        size = os.fstat(f.fileno()).st_size
+        _container.check_payload_size(size, off, count, TRIPLET_DTYPE.itemsize, _TRI_KIND)
+        stop = count if stop is None else min(stop, count)
+        pos = max(0, start)
+        f.seek(off + pos * TRIPLET_DTYPE.itemsize)
+        while pos < stop:
+            k = min(batch, stop - pos)
+            rec = np.fromfile(f, dtype=TRIPLET_DTYPE, count=k)
+            if rec.size < k:
+                raise CorruptInputError("triplet file truncated")
+            yield rec
+            pos += k
+
+
+def read_triplet_header(path) -> dict:
+    with open(path, "rb") as f:
+        header, count, _ = _container.read_preamble(f, TRI_MAGIC, _TRI_KIND)
+    header["count"] = count
+    return header
+
+
+def write_triplet_csv(path, triplets) -> None:
+    """CSV interchange form `dt,idx1,sim` (lsh_search.py:387-393)."""
+    if nat.is_device_tensor(triplets):
+        triplets = triplets.cpu().numpy().view(TRIPLET_DTYPE)
+    t = np.asarray(triplets, dtype=TRIPLET_DTYPE)
+    body = "".join(f"{a},{b},{c}\n" for a, b, c in zip(t["dt"].tolist(), t["idx1"].tolist(),
+                                                        t["sim"].tolist()))
+    with open(path, "w", encoding="utf-8") as f:
+        f.write("dt,idx1,sim\n")
+        f.write(body)
+
+
+def read_triplet_csv(path) -> np.ndarray:
+    with open(path, encoding="utf-8") as f:
+        head = f.readline().strip()
+        if head != "dt,idx1,sim":
+            raise CorruptInputError(f"unexpected triplet CSV header {head!r}")
+        rows = []
+        for line_no, line in enumerate(f, start=2):
+            line = line.strip()
+            if not line:
+                continue
+            parts = line.split(",")
+            if len(parts) != 3:
+                raise CorruptInputError(f"triplet CSV line {line_no} malformed")
+            try:
+                rows.append(tuple(int(v) for v in parts))
+            except ValueError as exc:
+                raise CorruptInputError(f"triplet CSV line {line_no}: {exc}") from exc
+    return np.array(rows, dtype=TRIPLET_DTYPE) if rows else np.empty(0, dtype=TRIPLET_DTYPE)

@@ -173,6 +173,33 @@ def fingerprint_cases():
     return cases
 
 
+def files():
+    """Artifacts written by the reference's own writers (lsh_search.py:339-393,
+    fingerprint.py:392-404, 529-551) -> tests/golden/files/."""
+    out = os.path.join(HERE, "files")
+    os.makedirs(out, exist_ok=True)
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal(30_000).astype(np.float32)
+    small = rfp.FingerprintParams(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=12,
+                                  top_k=24, stft=rfp.StftParams(frame_len_s=0.5, hop_s=0.05))
+    ts2 = TimeSeries("ST1", "HHZ", 100.0, 12.5, y)
+    fps2, mad2 = rfp.fingerprint_series(ts2, small, mad_rate=1.0)
+    rfp.write_fingerprint_file(os.path.join(out, "ref.fp"), fps2,
+                               extra={"config_hash": "abc123", "mad_seed": 0, "mad_rate": 1.0})
+    rfp.write_mad_file(os.path.join(out, "ref.mad"), mad2, extra={"station": "ST1"})
+    sigs = np.load(os.path.join(HERE, "search.npz"))["sigs7"]
+    cfg = rls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, occurrence_threshold=0.04)
+    rec, _ = rls.search_signatures(sigs, cfg)
+    header = {"config_hash": "abc123", "station": "ST1", "channel": "HHZ", "window_len_s": 3.0,
+              "window_lag_s": 0.5, "start_epoch_s": 12.5, "sorted": True}
+    rls.write_triplet_file(os.path.join(out, "ref.tri"), rec, header)
+    rls.write_triplet_csv(os.path.join(out, "ref.csv"), rec)
+    with open(os.path.join(out, "ref_inputs.json"), "w") as f:
+        json.dump({"tri_header": header, "n_triplets": int(rec.size)}, f, sort_keys=True)
+    for fn in sorted(os.listdir(out)):
+        print(fn, os.path.getsize(os.path.join(out, fn)))
+
+
 def main():
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1, sort_keys=True)
@@ -197,4 +224,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--files" in sys.argv:
+        files()
+    else:
+        main()
+        files()
