@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fingerprints", dest="n", type=int, default=8_000_000)
     ap.add_argument("--occ", type=float, default=1.5e-5, help="occurrence threshold (<=0: off)")
-    ap.add_argument("--ref-n", type=int, default=50_000)
+    ap.add_argument("--ref-n", type=int, default=100_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
@@ -186,7 +186,10 @@ def run_reference(args):
                                             "n": args.ref_n, "tables": 100, "hash_funcs": 4,
                                             "min_matches": 5},
             "cpu_baseline": {"value": value, "unit": "fingerprints/s", "cores": threads,
-                             "kind": kind, "sample": sample},
+                             "kind": kind, "sample": sample,
+                             "extrapolated_to_n": {"n": 8_000_000,
+                                                   "value": value * args.ref_n / 8_000_000,
+                                                   "law": "search time ~ N^2 (SURVEY 6.2)"}},
             "e2e": {"value": value, "unit": "fingerprints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -221,9 +224,11 @@ def fingerprint_bench(n_samples, steps, device):
     ms = a.elapsed_time(b) / steps
     # e2e: host float32 numpy trace in, host bits out
     tsh = TimeSeries("ST0", "HHZ", workloads.SR_HZ, 0.0, x)
+    fp.fingerprint_series(tsh, params, mad_rate=0.1)  # warm-up (pinned staging buffers)
     t0 = time.perf_counter()
-    fph, _ = fp.fingerprint_series(tsh, params, mad_rate=0.1)
-    e2e_s = time.perf_counter() - t0
+    for _ in range(steps):
+        fph, _ = fp.fingerprint_series(tsh, params, mad_rate=0.1)
+    e2e_s = (time.perf_counter() - t0) / steps
     return {"metric": "fingerprint Msamples/s", "value": n_samples / ms / 1e3, "unit": "Msamples/s",
             "ms_per_step": ms, "n_samples": n_samples, "n_fingerprints": int(len(fps)),
             "workload": "cfg0 (BASELINE.json configs[0]): 1 day at 100 Hz, 5 chirp templates x 20, "

@@ -208,6 +208,18 @@ int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_p
                     uint32_t key_bits, uint8_t* triplets_dev, void* ws_dev, size_t ws_bytes,
                     void* stream);
 
+/* Channel combine / triplet sort (align.py:87-140): n packed TRIPLET_DTYPE
+ * records (any order, several channels concatenated) are sorted by
+ * (dt, idx1); equal window pairs have their sims summed and sums below
+ * threshold dropped (threshold 0: plain sort, duplicates kept).  out_dev holds
+ * up to n records; *count_dev receives the number written.  key_bits = bits of
+ * (dt << 32 | idx1) that can be non-zero (64 if unknown).  QS_ERR_DATA when a
+ * dt or idx1 does not fit 32 bits. */
+size_t qs_triplets_combine_ws_bytes(uint64_t n);
+int qs_triplets_combine(const uint8_t* triplets_dev, uint64_t n, uint32_t threshold,
+                        uint32_t key_bits, uint8_t* out_dev, uint64_t* count_dev, void* ws_dev,
+                        size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ fingerprinting
  * Chain of fingerprint.fingerprint_series (fingerprint.py:581-623).  Float64
  * compute with float32 storage at the reference's rounding points

@@ -53,6 +53,14 @@ int cuda_status(cudaError_t e, const char* what);
         }                                                                  \
     } while (0)
 
+#define QS_DATA(cond, ...)                                                 \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            qs::set_error(__VA_ARGS__);                                    \
+            return QS_ERR_DATA;                                            \
+        }                                                                  \
+    } while (0)
+
 static inline unsigned qs_blocks(uint64_t n, unsigned threads, unsigned cap = 148u * 32u) {
     uint64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;

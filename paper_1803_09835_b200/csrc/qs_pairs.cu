@@ -707,6 +707,7 @@ __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* _
                            uint32_t tmax, uint64_t nb, uint32_t L,
                            const uint64_t* __restrict__ bigpos, uint64_t* __restrict__ bigb,
                            uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg) {
+    uint32_t mx = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = bsize[i];
@@ -715,8 +716,12 @@ __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* _
         const uint64_t nseg = (s + L - 1) / L;
         bigb[k] = i;
         bigcnt[k] = nseg * (nseg + 1) / 2;
-        atomicMax(maxnseg, (unsigned long long)nseg);
+        mx = max(mx, (uint32_t)nseg);
     }
+    // one atomic per warp (a single contended address otherwise serialises)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxnseg, (unsigned long long)mx);
 }
 
 __global__ void k_plan_bigitems(const uint32_t* __restrict__ bsize, const uint64_t* __restrict__ bigb,

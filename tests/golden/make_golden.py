@@ -194,6 +194,33 @@ def files():
               "window_lag_s": 0.5, "start_epoch_s": 12.5, "sorted": True}
     rls.write_triplet_file(os.path.join(out, "ref.tri"), rec, header)
     rls.write_triplet_csv(os.path.join(out, "ref.csv"), rec)
+    # channel combine + external sort (align.py:87-140) on three channels
+    from quakescan import align as ral
+    rng2 = np.random.default_rng(9)
+    pairs = rng2.integers(1, 40, size=(600, 2))
+    chans = []
+    for c in range(3):
+        sel = pairs[rng2.random(len(pairs)) < 0.5]
+        recc = np.zeros(len(sel), dtype=rls.TRIPLET_DTYPE)
+        recc["dt"], recc["idx1"] = sel[:, 0], sel[:, 1]
+        recc["sim"] = rng2.integers(1, 9, size=len(sel))
+        recc = recc[np.lexsort((recc["idx1"], recc["dt"]))]
+        # unique (dt, idx1) per channel, as a search emits
+        keep = np.ones(len(recc), bool)
+        keep[1:] = (recc["dt"][1:] != recc["dt"][:-1]) | (recc["idx1"][1:] != recc["idx1"][:-1])
+        recc = recc[keep]
+        pth = os.path.join(out, f"ch{c}.tri")
+        rls.write_triplet_file(pth, recc, {"channel": f"C{c}", "sorted": True})
+        chans.append(pth)
+    ral.combine_channel_triplets(chans, os.path.join(out, "combined.tri"), 6,
+                                 {"station": "ST1", "combined": True})
+    shuffled = np.fromfile(chans[0], dtype=np.uint8)
+    rec0, _ = rls.read_triplet_file(chans[0])
+    rls.write_triplet_file(os.path.join(out, "unsorted.tri"), rec0[rng2.permutation(len(rec0))],
+                           {"channel": "C0"})
+    ral.sort_triplet_file(os.path.join(out, "unsorted.tri"), os.path.join(out, "sorted.tri"),
+                          {"channel": "C0", "sorted": True}, chunk_records=50)
+    del shuffled
     with open(os.path.join(out, "ref_inputs.json"), "w") as f:
         json.dump({"tri_header": header, "n_triplets": int(rec.size)}, f, sort_keys=True)
     for fn in sorted(os.listdir(out)):
