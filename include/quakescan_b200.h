@@ -220,6 +220,16 @@ int qs_triplets_combine(const uint8_t* triplets_dev, uint64_t n, uint32_t thresh
                         uint32_t key_bits, uint8_t* out_dev, uint64_t* count_dev, void* ws_dev,
                         size_t ws_bytes, void* stream);
 
+/* Zero-phase band-pass (scipy.signal.sosfiltfilt with padtype "odd", as
+ * reference ingest.py:74-84 calls it): sos_host (n_sections x 6, a0 == 1) and
+ * zi_host (n_sections x 2, scipy.signal.sosfilt_zi) are small host arrays;
+ * x_dev / out_dev hold n float64 samples; pad = the odd-extension length.
+ * QS_ERR_ARG when n <= pad (scipy's ValueError). */
+size_t qs_sosfiltfilt_ws_bytes(uint64_t n, uint64_t pad);
+int qs_sosfiltfilt(const double* x_dev, uint64_t n, const double* sos_host, uint32_t n_sections,
+                   const double* zi_host, uint64_t pad, double* out_dev, void* ws_dev,
+                   size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ fingerprinting
  * Chain of fingerprint.fingerprint_series (fingerprint.py:581-623).  Float64
  * compute with float32 storage at the reference's rounding points

@@ -173,6 +173,25 @@ def fingerprint_cases():
     return cases
 
 
+def bandpass_cases():
+    """Reference ingest.bandpass (scipy sosfiltfilt) on seeded traces."""
+    from quakescan import ingest as ring
+    rng = np.random.default_rng(21)
+    out = {}
+    for name, (n, lo, hi, order, sr) in {
+        "cfg0_band": (60_000, 4.0, 10.0, 4, 100.0),
+        "wide_o2": (50_000, 1.0, 20.0, 2, 100.0),
+        "o8_short": (5_000, 2.0, 8.0, 8, 50.0),
+        "o1_min": (40, 5.0, 15.0, 1, 100.0),
+    }.items():
+        x = rng.standard_normal(n).astype(np.float32).astype(np.float64)
+        x += np.sin(np.arange(n) * 0.3) * 3.0
+        ts = TimeSeries("ST0", "HHZ", sr, 0.0, x)
+        y = ring.bandpass(ts, ring.BandpassSpec(lo, hi, order)).samples
+        out[name] = dict(x=x, y=y, spec=np.array([lo, hi, order, sr]))
+    return out
+
+
 def files():
     """Artifacts written by the reference's own writers (lsh_search.py:339-393,
     fingerprint.py:392-404, 529-551) -> tests/golden/files/."""
@@ -253,6 +272,10 @@ def main():
 if __name__ == "__main__":
     if "--files" in sys.argv:
         files()
+    elif "--bandpass" in sys.argv:
+        bp = bandpass_cases()
+        np.savez_compressed(os.path.join(HERE, "bandpass.npz"),
+                            **{f"{c}__{k}": v for c, d in bp.items() for k, v in d.items()})
     else:
         main()
         files()
