@@ -50,6 +50,14 @@ constexpr int QCAP = 64;
 #define QS_BUFKB 21
 #define QS_MINB 4
 #endif
+#ifndef QS_BUFKB_3
+#define QS_BUFKB_3 21
+#define QS_MINB_3 4
+#endif
+#ifndef QS_BUFKB_N
+#define QS_BUFKB_N 14
+#define QS_MINB_N 5
+#endif
 #ifndef QS_NBUF
 #define QS_NBUF 2
 #endif
@@ -87,8 +95,14 @@ struct TileCfg {
     static constexpr int ROW = W * NP;                        // u32 per staged row
     static constexpr int ROWP = ROW + 4;                      // padded stride: row-parallel
                                                               // 16-byte loads are conflict-free
-    static constexpr int BUFKB = MODE == MODE_MATCHED ? QS_BUFKB_M : QS_BUFKB;
-    static constexpr int MINB = MODE == MODE_MATCHED ? QS_MINB_M : QS_MINB;
+    // DISTINCT launches per table word with only words <= that word staged:
+    // narrow rows (W <= 2) run more CTAs with smaller buffers
+    static constexpr int BUFKB = MODE == MODE_MATCHED ? QS_BUFKB_M
+                               : (MODE == MODE_DISTINCT && W <= 2 ? QS_BUFKB_N
+                               : (MODE == MODE_DISTINCT && W == 3 ? QS_BUFKB_3 : QS_BUFKB));
+    static constexpr int MINB = MODE == MODE_MATCHED ? QS_MINB_M
+                              : (MODE == MODE_DISTINCT && W <= 2 ? QS_MINB_N
+                              : (MODE == MODE_DISTINCT && W == 3 ? QS_MINB_3 : QS_MINB));
     static constexpr int CAP = (BUFKB * 1024) / (ROWP * 4);  // rows per buffer
     static constexpr int L = CAP / 2;                         // small-bucket / segment limit
     static constexpr int MAXCH = L + (2 * L / 32 + 1) * (2 * L / (int)BPIECE + 1) + 16;
@@ -281,7 +295,7 @@ __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, ui
 
 template <int W, int NP>
 __device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const uint32_t* __restrict__ tags,
-                                          uint64_t n, uint32_t id) {
+                                          uint64_t n, uint32_t id, uint32_t wg) {
     uint4* dst = (uint4*)(rows + pos * (W * NP + 4));
 #pragma unroll
     for (int w = 0; w < W; ++w)
@@ -289,7 +303,7 @@ __device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const ui
         for (int qq = 0; qq < NP / 4; ++qq) {
             const uint32_t grp = qq >> 1;  // plane group (0: planes 0-7, 1: planes 8-15)
             cp_async16(dst + (w * (NP / 4) + qq),
-                       tags + ((uint64_t)grp * n + id) * W * 8 + w * 8 + (qq & 1) * 4);
+                       tags + ((uint64_t)grp * n + id) * wg * 8 + w * 8 + (qq & 1) * 4);
         }
 }
 
@@ -310,7 +324,9 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
     const uint64_t* __restrict__ rkeys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
     uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges,
     uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
-    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work, uint32_t tmax) {
+    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work, uint32_t tmax,
+    uint32_t wg) {
+    // W = tag words staged per row (words 0..W-1); wg = words per row in `tags`
     using C = TileCfg<W, MODE>;
     constexpr int NP = C::NP;
     constexpr uint32_t L = C::L;
@@ -481,7 +497,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                 uint32_t* rows = rowsb(b);
                 const uint32_t* ids = idsm(ma);
                 const uint32_t nrows = s_nrows[ma];
-                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r]);
+                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r], wg);
             }
             __syncwarp();
             mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
@@ -585,7 +601,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                         uint32_t s8 = 0;
                         if (w >= wt) {
                             s8 = pmask<W, NP>(A, R, w, 8);
-                            if (w == W - 1) s8 &= last_mask;
+                            if (w == (int)wg - 1) s8 &= last_mask;
                             cnt += __popc(w == wt ? (s8 & ~((low << 1) | 1u)) : s8);
                         }
                         qmask[w] = s8;
@@ -599,12 +615,12 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                         uint32_t x = 0;
                         if (w <= wt) {
                             x = pmask<W, NP>(A, R, w, 16);
-                            if (w == W - 1) x &= last_mask;
+                            if (w == (int)wg - 1) x &= last_mask;
                             early |= (w < wt) ? x : (x & low);
                             if (w == wt) cnt += __popc(x & ~low);
                         } else if (MODE == MODE_FULL) {
                             x = pmask<W, NP>(A, R, w, 8);
-                            if (w == W - 1) x &= last_mask;
+                            if (w == (int)wg - 1) x &= last_mask;
                             cnt += __popc(x);
                         }
                         qmask[w] = x;
@@ -858,7 +874,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
                   uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
                   const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
                   uint64_t cap, unsigned long long* counters, uint64_t* ws, void* sws,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint32_t wg) {
     using C = TileCfg<W, MODE>;
     const uint32_t L = C::L;
     uint64_t* mpre = ws;                       // nb + 1
@@ -896,8 +912,55 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     if (per_sm < 1) per_sm = 1;
     kern<<<num_sms() * per_sm, PTHREADS, C::SMEM, st>>>(sids, bstart, bsize, btab, plan, rkeys, tags,
                                                         n, t, m, excl, emask, edges, p, out_key,
-                                                        out_sim, cap, counters, work, tmax);
+                                                        out_sim, cap, counters, work, tmax, wg);
     QS_CHECK_LAUNCH("k_pairs_pc");
+    return QS_OK;
+}
+
+// first bucket of each table word (btab is non-decreasing): bounds[w] for w <= W
+__global__ void k_word_bounds(const uint32_t* __restrict__ btab, uint64_t nb, uint32_t W,
+                              uint64_t* __restrict__ bounds) {
+    const uint32_t w = threadIdx.x;
+    if (w > W) return;
+    uint64_t lo = 0, hi = nb;
+    const uint32_t target = w * 32;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (btab[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[w] = w == W ? nb : lo;
+}
+
+// DISTINCT: one launch per table word w over that word's buckets, staging only
+// tag words 0..w (the first-collision test never reads later words)
+template <int W, bool HAS_E>
+static int run_distinct_split(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
+                              const uint32_t* btab, uint64_t nb, const uint64_t* rkeys,
+                              const uint32_t* tags, uint64_t n, uint32_t t, uint32_t m,
+                              uint64_t excl, const uint8_t* emask, const uint64_t* edges,
+                              uint32_t p, uint64_t* ok, uint32_t* os, uint64_t cap,
+                              unsigned long long* counters, uint64_t* ws, void* sws,
+                              cudaStream_t st) {
+    uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
+    k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
+    uint64_t hb[5] = {0, 0, 0, 0, 0};
+    QS_CUDA(cudaMemcpyAsync(hb, dbounds, (W + 1) * 8, cudaMemcpyDeviceToHost, st), "copy");
+    QS_CUDA(cudaStreamSynchronize(st), "sync");
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint64_t a = hb[w], b = hb[w + 1];
+        if (b <= a) continue;
+#define QS_W(WS)                                                                                   \
+    run_pc<WS, MODE_DISTINCT, HAS_E>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
+                                     m, excl, emask, edges, p, ok, os, cap, counters, ws, sws, st, W)
+        int rc = QS_OK;
+        if (w == 0) rc = QS_W(1);
+        else if (w == 1) { if constexpr (W >= 2) rc = QS_W(2); }
+        else if (w == 2) { if constexpr (W >= 3) rc = QS_W(3); }
+        else { if constexpr (W >= 4) rc = QS_W(4); }
+#undef QS_W
+        if (rc) return rc;
+    }
     return QS_OK;
 }
 
@@ -910,11 +973,15 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
                          unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
 #define QS_L(MM, EE) \
     run_pc<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, p, \
-                      ok, os, cap, counters, ws, sws, st)
+                      ok, os, cap, counters, ws, sws, st, W)
+#define QS_D(EE) \
+    run_distinct_split<W, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
+                              edges, p, ok, os, cap, counters, ws, sws, st)
     if (mode == MODE_FULL) return has_e ? QS_L(MODE_FULL, true) : QS_L(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_L(MODE_MATCHED, true) : QS_L(MODE_MATCHED, false);
-    return has_e ? QS_L(MODE_DISTINCT, true) : QS_L(MODE_DISTINCT, false);
+    return has_e ? QS_D(true) : QS_D(false);
 #undef QS_L
+#undef QS_D
 }
 
 }  // namespace qs
