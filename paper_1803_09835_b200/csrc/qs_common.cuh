@@ -27,6 +27,11 @@ __host__ __device__ __forceinline__ uint64_t combine1(uint64_t acc, uint64_t w) 
     return acc ^ (fmix64(w) + GOLDEN64 + (acc << 6) + (acc >> 2));
 }
 
+// The same step with fmix64(w) precomputed (the Min-Max plan stores mixed values).
+__host__ __device__ __forceinline__ uint64_t combine1_mixed(uint64_t acc, uint64_t fw) {
+    return acc ^ (fw + GOLDEN64 + (acc << 6) + (acc >> 2));
+}
+
 // Per-thread last error text, retrievable through qs_last_error().
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);

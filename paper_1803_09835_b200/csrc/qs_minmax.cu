@@ -30,7 +30,8 @@ constexpr uint32_t PLAN_MAX_D = 16384;  // smem bitonic sort capacity (192 KB)
 
 // Plan layout, probe-sequence-major so one probe sequence walks consecutive
 // addresses (L1-resident prefixes): order[side][f][r], svals[side][f][r] with
-// side 0 = ascending value order (minimum probes), side 1 = descending (maximum).
+// side 0 = ascending value order (minimum probes), side 1 = descending (maximum);
+// svals holds fmix64(value), the only form the combine step uses.
 static inline size_t plan_order_bytes(uint32_t d, uint32_t F) {
     return (((size_t)2 * d * F * sizeof(uint16_t)) + 255) & ~(size_t)255;
 }
@@ -75,10 +76,11 @@ __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, u
     }
     for (uint32_t r = threadIdx.x; r < d; r += blockDim.x) {
         const uint64_t up = (uint64_t)f * d + r, down = ((uint64_t)F + f) * d + r;
+        // the combine step only ever uses fmix64(value): store it pre-mixed
         order[up] = (uint16_t)idx[r];
-        svals[up] = key[r];
+        svals[up] = fmix64(key[r]);
         order[down] = (uint16_t)idx[d - 1 - r];
-        svals[down] = key[d - 1 - r];
+        svals[down] = fmix64(key[d - 1 - r]);
     }
 }
 
@@ -179,11 +181,11 @@ __global__ void __launch_bounds__(256) k_signatures(
             if (i < t) {
                 for (uint32_t j = 0; j < kh; ++j) {
                     const uint32_t sq = i * kh + j;
-                    acc = combine1(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
+                    acc = combine1_mixed(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
                 }
                 for (uint32_t j = 0; j < kh; ++j) {
                     const uint32_t sq = F + i * kh + j;
-                    acc = combine1(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
+                    acc = combine1_mixed(acc, __ldg(svals + (uint64_t)sq * d + rk[sq]));
                 }
                 if (sigs) sigs[row * t + i] = acc;
             }
