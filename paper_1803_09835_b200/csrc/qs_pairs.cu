@@ -89,20 +89,35 @@ __device__ unsigned long long g_prof[8];
 #define PROF_FLUSH(base)
 #endif
 
-template <int W, int MODE>
+// Staged row layout of a launch: tag planes kept per 32-table word.  MATCHED
+// screens with planes 0-7 of every word; DISTINCT (one launch per table word
+// WT, W = WT + 1) needs all 16 planes of words <= WT; FULL (one launch per
+// word WT) needs 16 planes of words <= WT (first-table test) and 8 of the
+// later words (count screen).
+template <int MODE, int WT>
+struct Layout {
+    static constexpr int planes(int w) {
+        return MODE == MODE_MATCHED ? 8 : (MODE == MODE_DISTINCT ? 16 : (w <= WT ? 16 : 8));
+    }
+    static constexpr int off(int w) {  // closed form: folds to an immediate in unrolled loops
+        return MODE == MODE_MATCHED ? 8 * w
+             : (MODE == MODE_DISTINCT || w <= WT + 1 ? 16 * w : 16 * (WT + 1) + 8 * (w - WT - 1));
+    }
+};
+
+template <int W, int MODE, int WT>
 struct TileCfg {
-    static constexpr int NP = MODE == MODE_MATCHED ? 8 : 16;  // planes staged / in registers
-    static constexpr int ROW = W * NP;                        // u32 per staged row
+    using Lay = Layout<MODE, WT>;
+    static constexpr int NP = MODE == MODE_MATCHED ? 8 : 16;  // max planes per word (registers)
+    static constexpr int ROW = Lay::off(W);                   // u32 per staged row
     static constexpr int ROWP = ROW + 4;                      // padded stride: row-parallel
                                                               // 16-byte loads are conflict-free
     // DISTINCT launches per table word with only words <= that word staged:
     // narrow rows (W <= 2) run more CTAs with smaller buffers
     static constexpr int BUFKB = MODE == MODE_MATCHED ? QS_BUFKB_M
-                               : (MODE == MODE_DISTINCT && W <= 2 ? QS_BUFKB_N
-                               : (MODE == MODE_DISTINCT && W == 3 ? QS_BUFKB_3 : QS_BUFKB));
+                               : (ROW <= 32 ? QS_BUFKB_N : (ROW <= 48 ? QS_BUFKB_3 : QS_BUFKB));
     static constexpr int MINB = MODE == MODE_MATCHED ? QS_MINB_M
-                              : (MODE == MODE_DISTINCT && W <= 2 ? QS_MINB_N
-                              : (MODE == MODE_DISTINCT && W == 3 ? QS_MINB_3 : QS_MINB));
+                              : (ROW <= 32 ? QS_MINB_N : (ROW <= 48 ? QS_MINB_3 : QS_MINB));
     static constexpr int CAP = (BUFKB * 1024) / (ROWP * 4);  // rows per buffer
     static constexpr int L = CAP / 2;                         // small-bucket / segment limit
     static constexpr int MAXCH = L + (2 * L / 32 + 1) * (2 * L / (int)BPIECE + 1) + 16;
@@ -164,9 +179,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // (uniform across the warp: broadcast shared-memory reads, immediate offsets).
 template <int W, int NP>
 __device__ __forceinline__ uint32_t pmask(const uint32_t (&A)[W][NP], const uint32_t* R, int w,
-                                          int np) {
+                                          int np, int woff) {
     uint32_t x = 0xFFFFFFFFu;
-    const uint4* r4 = (const uint4*)(R + w * NP);
+    const uint4* r4 = (const uint4*)(R + woff);
 #pragma unroll
     for (int q = 0; q < NP / 4; ++q) {
         if (q * 4 >= np) break;
@@ -293,16 +308,16 @@ __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, ui
     }
 }
 
-template <int W, int NP>
+template <int W, class Lay, int ROWP>
 __device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const uint32_t* __restrict__ tags,
                                           uint64_t n, uint32_t id, uint32_t wg) {
-    uint4* dst = (uint4*)(rows + pos * (W * NP + 4));
+    uint4* dst = (uint4*)(rows + pos * ROWP);
 #pragma unroll
     for (int w = 0; w < W; ++w)
 #pragma unroll
-        for (int qq = 0; qq < NP / 4; ++qq) {
+        for (int qq = 0; qq < Lay::planes(w) / 4; ++qq) {
             const uint32_t grp = qq >> 1;  // plane group (0: planes 0-7, 1: planes 8-15)
-            cp_async16(dst + (w * (NP / 4) + qq),
+            cp_async16(dst + (Lay::off(w) / 4 + qq),
                        tags + ((uint64_t)grp * n + id) * wg * 8 + w * 8 + (qq & 1) * 4);
         }
 }
@@ -317,8 +332,8 @@ struct Plan {
                                  // [4] max segments per bucket, [5] item table valid
 };
 
-template <int W, int MODE, bool HAS_E>
-__global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
+template <int W, int MODE, bool HAS_E, int WT>
+__global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_pc(
     const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
     const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab, Plan plan,
     const uint64_t* __restrict__ rkeys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
@@ -326,8 +341,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
     uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
     unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work, uint32_t tmax,
     uint32_t wg) {
-    // W = tag words staged per row (words 0..W-1); wg = words per row in `tags`
-    using C = TileCfg<W, MODE>;
+    // W = tag words staged per row (words 0..W-1); wg = words per row in `tags`;
+    // WT = the launch's table word (DISTINCT / FULL are launched per word)
+    using C = TileCfg<W, MODE, WT>;
+    using Lay = typename C::Lay;
     constexpr int NP = C::NP;
     constexpr uint32_t L = C::L;
     extern __shared__ __align__(128) unsigned char psm[];
@@ -497,7 +514,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                 uint32_t* rows = rowsb(b);
                 const uint32_t* ids = idsm(ma);
                 const uint32_t nrows = s_nrows[ma];
-                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, NP>(rows, r, tags, n, ids[r], wg);
+                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, Lay, C::ROWP>(rows, r, tags, n, ids[r], wg);
             }
             __syncwarp();
             mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
@@ -563,8 +580,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
 #pragma unroll
                 for (int w = 0; w < W; ++w)
 #pragma unroll
-                    for (int qq = 0; qq < NP / 4; ++qq) {
-                        const uint4 v = src[w * (NP / 4) + qq];
+                    for (int qq = 0; qq < Lay::planes(w) / 4; ++qq) {
+                        const uint4 v = src[Lay::off(w) / 4 + qq];
                         A[w][qq * 4 + 0] = v.x; A[w][qq * 4 + 1] = v.y;
                         A[w][qq * 4 + 2] = v.z; A[w][qq * 4 + 3] = v.w;
                     }
@@ -600,7 +617,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                     for (int w = 0; w < W; ++w) {
                         uint32_t s8 = 0;
                         if (w >= wt) {
-                            s8 = pmask<W, NP>(A, R, w, 8);
+                            s8 = pmask<W, NP>(A, R, w, 8, Lay::off(w));
                             if (w == (int)wg - 1) s8 &= last_mask;
                             cnt += __popc(w == wt ? (s8 & ~((low << 1) | 1u)) : s8);
                         }
@@ -613,13 +630,13 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
                         uint32_t x = 0;
-                        if (w <= wt) {
-                            x = pmask<W, NP>(A, R, w, 16);
+                        if (w <= WT) {  // launches are per table word: wt == WT
+                            x = pmask<W, NP>(A, R, w, 16, Lay::off(w));
                             if (w == (int)wg - 1) x &= last_mask;
-                            early |= (w < wt) ? x : (x & low);
-                            if (w == wt) cnt += __popc(x & ~low);
+                            early |= (w < WT) ? x : (x & low);
+                            if (w == WT) cnt += __popc(x & ~low);
                         } else if (MODE == MODE_FULL) {
-                            x = pmask<W, NP>(A, R, w, 8);
+                            x = pmask<W, NP>(A, R, w, 8, Lay::off(w));
                             if (w == (int)wg - 1) x &= last_mask;
                             cnt += __popc(x);
                         }
@@ -648,7 +665,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE>::MINB) k_pairs_pc(
                     if (MODE == MODE_MATCHED) {
 #pragma unroll
                         for (int w = 0; w < W; ++w)
-                            if (w < wt) qmask[w] = pmask<W, NP>(A, R, w, 8);
+                            if (w < wt) qmask[w] = pmask<W, NP>(A, R, w, 8, Lay::off(w));
                     }
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
@@ -868,14 +885,14 @@ __global__ void k_chunk_counts(const uint32_t* __restrict__ bsize, uint64_t nb,
 }
 
 // ------------------------------------------------------------------ launch
-template <int W, int MODE, bool HAS_E>
+template <int W, int MODE, bool HAS_E, int WT>
 static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
                   const uint32_t* btab, uint64_t nb, const uint64_t* rkeys, const uint32_t* tags,
                   uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
                   const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
                   uint64_t cap, unsigned long long* counters, uint64_t* ws, void* sws,
                   cudaStream_t st, uint32_t wg) {
-    using C = TileCfg<W, MODE>;
+    using C = TileCfg<W, MODE, WT>;
     const uint32_t L = C::L;
     uint64_t* mpre = ws;                       // nb + 1
     uint64_t* bigpos = mpre + (nb + 1);        // nb + 1
@@ -904,7 +921,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
     QS_CHECK_LAUNCH("plan");
     Plan plan{mpre, tile_first, items, bigb, bigoff, totals};
-    auto kern = k_pairs_pc<W, MODE, HAS_E>;
+    auto kern = k_pairs_pc<W, MODE, HAS_E, WT>;
     QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM),
             "smem attr");
     int per_sm = 1;
@@ -932,16 +949,16 @@ __global__ void k_word_bounds(const uint32_t* __restrict__ btab, uint64_t nb, ui
     bounds[w] = w == W ? nb : lo;
 }
 
-// DISTINCT: one launch per table word w over that word's buckets, staging only
-// tag words 0..w (the first-collision test never reads later words)
-template <int W, bool HAS_E>
-static int run_distinct_split(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
-                              const uint32_t* btab, uint64_t nb, const uint64_t* rkeys,
-                              const uint32_t* tags, uint64_t n, uint32_t t, uint32_t m,
-                              uint64_t excl, const uint8_t* emask, const uint64_t* edges,
-                              uint32_t p, uint64_t* ok, uint32_t* os, uint64_t cap,
-                              unsigned long long* counters, uint64_t* ws, void* sws,
-                              cudaStream_t st) {
+// DISTINCT / FULL: one launch per table word w over that word's buckets.
+// DISTINCT stages only words 0..w (16 planes); FULL stages words 0..w with 16
+// planes and the later words with 8 (count screen).
+template <int W, int MODE, bool HAS_E>
+static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const uint32_t* bsize,
+                          const uint32_t* btab, uint64_t nb, const uint64_t* rkeys,
+                          const uint32_t* tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
+                          const uint8_t* emask, const uint64_t* edges, uint32_t p, uint64_t* ok,
+                          uint32_t* os, uint64_t cap, unsigned long long* counters, uint64_t* ws,
+                          void* sws, cudaStream_t st) {
     uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
     k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
     uint64_t hb[5] = {0, 0, 0, 0, 0};
@@ -950,14 +967,20 @@ static int run_distinct_split(const uint32_t* sids, const uint64_t* bstart, cons
     for (uint32_t w = 0; w < W; ++w) {
         const uint64_t a = hb[w], b = hb[w + 1];
         if (b <= a) continue;
-#define QS_W(WS)                                                                                   \
-    run_pc<WS, MODE_DISTINCT, HAS_E>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
-                                     m, excl, emask, edges, p, ok, os, cap, counters, ws, sws, st, W)
+#define QS_W(WW, WTT)                                                                             \
+    run_pc<WW, MODE, HAS_E, WTT>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
+                                 m, excl, emask, edges, p, ok, os, cap, counters, ws, sws, st, W)
+        constexpr bool DI = MODE == MODE_DISTINCT;
         int rc = QS_OK;
-        if (w == 0) rc = QS_W(1);
-        else if (w == 1) { if constexpr (W >= 2) rc = QS_W(2); }
-        else if (w == 2) { if constexpr (W >= 3) rc = QS_W(3); }
-        else { if constexpr (W >= 4) rc = QS_W(4); }
+        if (w == 0) {
+            if constexpr (DI) rc = QS_W(1, 0); else rc = QS_W(W, 0);
+        } else if (w == 1) {
+            if constexpr (W >= 2) { if constexpr (DI) rc = QS_W(2, 1); else rc = QS_W(W, 1); }
+        } else if (w == 2) {
+            if constexpr (W >= 3) { if constexpr (DI) rc = QS_W(3, 2); else rc = QS_W(W, 2); }
+        } else {
+            if constexpr (W >= 4) { if constexpr (DI) rc = QS_W(4, 3); else rc = QS_W(W, 3); }
+        }
 #undef QS_W
         if (rc) return rc;
     }
@@ -972,14 +995,14 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
                          uint32_t p, uint64_t* ok, uint32_t* os, uint64_t cap,
                          unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
 #define QS_L(MM, EE) \
-    run_pc<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, p, \
-                      ok, os, cap, counters, ws, sws, st, W)
-#define QS_D(EE) \
-    run_distinct_split<W, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
+    run_pc<W, MM, EE, 0>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, \
+                         p, ok, os, cap, counters, ws, sws, st, W)
+#define QS_D(MM, EE) \
+    run_word_split<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
                               edges, p, ok, os, cap, counters, ws, sws, st)
-    if (mode == MODE_FULL) return has_e ? QS_L(MODE_FULL, true) : QS_L(MODE_FULL, false);
+    if (mode == MODE_FULL) return has_e ? QS_D(MODE_FULL, true) : QS_D(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_L(MODE_MATCHED, true) : QS_L(MODE_MATCHED, false);
-    return has_e ? QS_D(true) : QS_D(false);
+    return has_e ? QS_D(MODE_DISTINCT, true) : QS_D(MODE_DISTINCT, false);
 #undef QS_L
 #undef QS_D
 }
