@@ -616,10 +616,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
 #pragma unroll
                     for (int w = 0; w < W; ++w) {
                         uint32_t s8 = 0;
-                        if (w >= wt) {
+                        if (w >= WT) {  // launches are per table word: wt == WT
                             s8 = pmask<W, NP>(A, R, w, 8, Lay::off(w));
                             if (w == (int)wg - 1) s8 &= last_mask;
-                            cnt += __popc(w == wt ? (s8 & ~((low << 1) | 1u)) : s8);
+                            cnt += __popc(w == WT ? (s8 & ~((low << 1) | 1u)) : s8);
                         }
                         qmask[w] = s8;
                     }
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     if (MODE == MODE_MATCHED) {
 #pragma unroll
                         for (int w = 0; w < W; ++w)
-                            if (w < wt) qmask[w] = pmask<W, NP>(A, R, w, 8, Lay::off(w));
+                            if (w < WT) qmask[w] = pmask<W, NP>(A, R, w, 8, Lay::off(w));
                     }
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
@@ -967,6 +967,7 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
     for (uint32_t w = 0; w < W; ++w) {
         const uint64_t a = hb[w], b = hb[w + 1];
         if (b <= a) continue;
+        if (MODE == MODE_MATCHED && 32 * w > t - m) continue;  // no first collision there
 #define QS_W(WW, WTT)                                                                             \
     run_pc<WW, MODE, HAS_E, WTT>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
                                  m, excl, emask, edges, p, ok, os, cap, counters, ws, sws, st, W)
@@ -1001,7 +1002,7 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
     run_word_split<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
                               edges, p, ok, os, cap, counters, ws, sws, st)
     if (mode == MODE_FULL) return has_e ? QS_D(MODE_FULL, true) : QS_D(MODE_FULL, false);
-    if (mode == MODE_MATCHED) return has_e ? QS_L(MODE_MATCHED, true) : QS_L(MODE_MATCHED, false);
+    if (mode == MODE_MATCHED) return has_e ? QS_D(MODE_MATCHED, true) : QS_D(MODE_MATCHED, false);
     return has_e ? QS_D(MODE_DISTINCT, true) : QS_D(MODE_DISTINCT, false);
 #undef QS_L
 #undef QS_D
