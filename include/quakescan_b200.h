@@ -202,7 +202,9 @@ int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_d
                         uint32_t* out_sim_dev, unsigned long long* counter_dev, void* stream);
 
 /* Sort matched pairs by (dt, idx1) (lsh_search.py:291) and pack them into
- * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38). */
+ * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38).
+ * key_bits = 32 + b where both dt and idx1 are < 2^b (b = bit length of n):
+ * digits that are zero in both halves are not sorted on. */
 size_t qs_sort_pairs_ws_bytes(uint64_t n);
 int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_pairs,
                     uint32_t key_bits, uint8_t* triplets_dev, void* ws_dev, size_t ws_bytes,

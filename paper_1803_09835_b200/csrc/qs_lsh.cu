@@ -971,7 +971,8 @@ int qs_lsh_finalize(uint64_t* pair_key_dev, uint32_t* pair_sim_dev, uint64_t n_p
     void* rws = (void*)(((uintptr_t)(w + n_pairs * 12) + 255) & ~(uintptr_t)255);
     int in_alt = 0;
     int rc = radix_sort_pairs(pair_key_dev, pair_sim_dev, n_pairs, 1, key_bits, ak, av, rws,
-                              radix_ws_bytes(n_pairs, 1), &in_alt, st);
+                              radix_ws_bytes(n_pairs, 1), &in_alt, st, 0,
+                              key_bits > 32 ? key_bits - 32 : 32);
     if (rc) return rc;
     const uint64_t* k = in_alt ? ak : pair_key_dev;
     const uint32_t* v = in_alt ? av : pair_sim_dev;

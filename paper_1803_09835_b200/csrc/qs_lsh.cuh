@@ -7,7 +7,8 @@ namespace qs {
 
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
                      uint32_t key_bits, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
-                     size_t ws_bytes, int* in_alt, cudaStream_t st, uint32_t bit_lo = 0);
+                     size_t ws_bytes, int* in_alt, cudaStream_t st, uint32_t bit_lo = 0,
+                     uint32_t lo_bits = 32);
 size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments);
 int radix_sort_pairs_to(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t seg_len,
                         uint32_t segments, uint32_t bit_lo, uint32_t key_bits, uint64_t* keys_out,

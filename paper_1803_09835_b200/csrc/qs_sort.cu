@@ -191,7 +191,8 @@ size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments) {
 
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
                      uint32_t key_bits, uint64_t* keys_alt, uint32_t* vals_alt, void* ws,
-                     size_t ws_bytes, int* in_alt, cudaStream_t st, uint32_t bit_lo) {
+                     size_t ws_bytes, int* in_alt, cudaStream_t st, uint32_t bit_lo,
+                     uint32_t lo_bits) {
     *in_alt = 0;
     if (seg_len == 0 || segments == 0 || key_bits == 0) return QS_OK;
     QS_ARG(seg_len < (1ull << 32), "radix sort segment longer than 2^32");
@@ -203,7 +204,10 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t 
                                  RS_TILE * 12), "smem attr");
     uint64_t *src_k = keys, *dst_k = keys_alt;
     uint32_t *src_v = vals, *dst_v = vals_alt;
+    // lo_bits < 32: the low 32-bit half only uses its lowest lo_bits bits (a
+    // (dt << 32 | idx1) pair key): its always-zero digits are skipped
     for (uint32_t shift = bit_lo; shift < key_bits; shift += 8) {
+        if (shift < 32 && shift >= lo_bits) continue;
         dim3 grid(tiles, segments);
         k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
         k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
@@ -268,7 +272,7 @@ int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len
     QS_ARG(key_bits <= 64, "key_bits must be <= 64");
     return qs::radix_sort_pairs(keys_dev, vals_dev, seg_len, segments, key_bits, keys_alt_dev,
                                 vals_alt_dev, ws_dev, ws_bytes, result_in_alt,
-                                (cudaStream_t)stream, 0);
+                                (cudaStream_t)stream, 0, 32);
 }
 
 }  // extern "C"

@@ -257,7 +257,11 @@ class DeviceSearch:
                      nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n, self.t, m, excl,
                      nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk), nat.ptr(ps), cap,
                      nat.ptr(counters), nat.ptr(ws), ws.numel(), nat.stream())
-            self.launches += 5
+            # word bounds + per launched table word: 7 planning kernels, 2x3 scan kernels, pairs
+            words = (self.t + 31) // 32
+            if mode == self.MODE_MATCHED:
+                words = min(words, (self.t - m) // 32 + 1)
+            self.launches += 1 + 14 * words
             distinct, matched = (int(v) for v in counters.tolist())
             if matched <= cap:
                 break
