@@ -117,7 +117,17 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         k[r] = ok ? keys[base + i] : 0;
         v[r] = ok ? (vals ? vals[base + i] : (uint32_t)i) : 0;  // no vals: in-segment position
         const uint32_t dgt = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : 0x100u;
+#ifdef QS_RS_BALLOT
+        uint32_t peers = 0xffffffffu;  // lanes with the same digit, from 9 ballots
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+            const bool bit = (dgt >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+#else
         const uint32_t peers = __match_any_sync(0xffffffffu, dgt);
+#endif
         const uint32_t cnt = __popc(peers);
         const uint32_t before = __popc(peers & lt);
         uint32_t b = 0;
