@@ -83,6 +83,92 @@ __global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* __restrict__ hist, u
     }
 }
 
+// Multi-block exclusive scan of one long uint32 histogram (single-segment
+// sorts: a lone CTA would walk 256 x tiles entries serially).
+constexpr int RSC_T = 512, RSC_I = 8;
+constexpr uint64_t RSC_TILE = (uint64_t)RSC_T * RSC_I;
+
+__device__ __forceinline__ uint64_t rs_block_excl(uint64_t v, uint64_t* wsum) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (uint32_t)o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t r = (warp ? wsum[warp - 1] : 0) + x - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(RSC_T) k_rs_scan_reduce(const uint32_t* __restrict__ a, uint64_t len,
+                                                          uint64_t* __restrict__ part) {
+    __shared__ uint64_t red[RSC_T / 32];
+    const uint64_t base = blockIdx.x * RSC_TILE;
+    uint64_t s = 0;
+    for (int e = 0; e < RSC_I; ++e) {
+        const uint64_t i = base + (uint64_t)e * RSC_T + threadIdx.x;
+        if (i < len) s += a[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < RSC_T / 32; ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_rs_scan_top(uint64_t* __restrict__ part, uint64_t nb) {
+    __shared__ uint64_t ws[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < nb; b0 += 1024) {
+        const uint64_t i = b0 + threadIdx.x;
+        const uint64_t v = i < nb ? part[i] : 0;
+        const uint64_t ex = rs_block_excl(v, ws);
+        const uint64_t tot = ws[31];
+        if (i < nb) part[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(RSC_T) k_rs_scan_down(uint32_t* __restrict__ a, uint64_t len,
+                                                        const uint64_t* __restrict__ part) {
+    __shared__ uint64_t ws[32];
+    const uint64_t base = blockIdx.x * RSC_TILE + (uint64_t)threadIdx.x * RSC_I;
+    uint32_t v[RSC_I];
+    uint64_t s = 0;
+#pragma unroll
+    for (int e = 0; e < RSC_I; ++e) {
+        v[e] = (base + e < len) ? a[base + e] : 0u;
+        s += v[e];
+    }
+    uint64_t ex = rs_block_excl(s, ws) + part[blockIdx.x];
+#pragma unroll
+    for (int e = 0; e < RSC_I; ++e) {
+        if (base + e < len) a[base + e] = (uint32_t)ex;
+        ex += v[e];
+    }
+}
+
 // Stable scatter of one tile: rank in input order per digit, stage the tile in
 // shared memory in (digit, input) order, then write each digit's run to its
 // global slot with consecutive threads on consecutive addresses (coalesced).
@@ -117,7 +203,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         k[r] = ok ? keys[base + i] : 0;
         v[r] = ok ? (vals ? vals[base + i] : (uint32_t)i) : 0;  // no vals: in-segment position
         const uint32_t dgt = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : 0x100u;
-#ifdef QS_RS_BALLOT
+#ifndef QS_RS_MATCH
         uint32_t peers = 0xffffffffu;  // lanes with the same digit, from 9 ballots
 #pragma unroll
         for (int b = 0; b < 9; ++b) {
@@ -196,7 +282,23 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
 static uint32_t rs_tiles(uint64_t seg_len) { return (uint32_t)((seg_len + RS_TILE - 1) / RS_TILE); }
 
 size_t radix_ws_bytes(uint64_t seg_len, uint32_t segments) {
-    return (size_t)rs_tiles(seg_len) * RS_RADIX * segments * sizeof(uint32_t) + 256;
+    const uint64_t hist = (uint64_t)rs_tiles(seg_len) * RS_RADIX * segments;
+    return (size_t)hist * sizeof(uint32_t) + ((hist + RSC_TILE - 1) / RSC_TILE + 1) * 8 + 512;
+}
+
+// per-segment exclusive scans of the digit histograms
+static void rs_scan(uint32_t* hist, uint64_t seg_hist, uint32_t segments, void* ws,
+                    cudaStream_t st) {
+    if (segments > 1 || seg_hist < (1u << 18)) {
+        k_rs_scan<<<segments, 1024, 0, st>>>(hist, seg_hist);
+        return;
+    }
+    const uint64_t nb = (seg_hist + RSC_TILE - 1) / RSC_TILE;
+    uint64_t* part = (uint64_t*)(((uintptr_t)(hist + seg_hist) + 15) & ~(uintptr_t)15);
+    (void)ws;
+    k_rs_scan_reduce<<<(unsigned)nb, RSC_T, 0, st>>>(hist, seg_hist, part);
+    k_rs_scan_top<<<1, 1024, 0, st>>>(part, nb);
+    k_rs_scan_down<<<(unsigned)nb, RSC_T, 0, st>>>(hist, seg_hist, part);
 }
 
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t segments,
@@ -220,7 +322,7 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t seg_len, uint32_t 
         if (shift < 32 && shift >= lo_bits) continue;
         dim3 grid(tiles, segments);
         k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
-        k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
+        rs_scan(hist, (uint64_t)RS_RADIX * tiles, segments, ws, st);
         k_rs_scatter<<<grid, RS_THREADS, RS_TILE * 12, st>>>(src_k, src_v, seg_len, tiles, shift,
                                                              hist, dst_k, dst_v);
         QS_CHECK_LAUNCH("radix sort pass");
@@ -257,7 +359,7 @@ int radix_sort_pairs_to(const uint64_t* keys_in, const uint32_t* vals_in, uint64
         uint32_t* dst_v = to_out ? vals_out : vals_alt;
         dim3 grid(tiles, segments);
         k_rs_hist<<<grid, RS_THREADS, 0, st>>>(src_k, seg_len, tiles, shift, hist);
-        k_rs_scan<<<segments, 1024, 0, st>>>(hist, (uint64_t)RS_RADIX * tiles);
+        rs_scan(hist, (uint64_t)RS_RADIX * tiles, segments, ws, st);
         k_rs_scatter<<<grid, RS_THREADS, RS_TILE * 12, st>>>(src_k, src_v, seg_len, tiles, shift,
                                                              hist, dst_k, dst_v);
         QS_CHECK_LAUNCH("radix sort pass");
