@@ -119,3 +119,52 @@ def test_search_config_validation(ls):
     with pytest.raises(ParameterError):
         ls.search_signatures(np.zeros((3, 4), np.uint64), ls.SearchConfig(tables=5))
     assert ls.PROFILES == {"baseline": (6, 5), "optimized": (8, 2)}
+
+
+def _check_triplets_against_keys(rec_dev, rkeys, n, m):
+    """Size-independent properties of an emitted triplet set: sorted by
+    (dt, idx1) without duplicates, dt >= 1, both ends in range, sim >= m and
+    sim == the number of tables whose keys agree (recomputed from the keys)."""
+    import torch
+    cnt = rec_dev.numel() // 20
+    if cnt == 0:
+        return
+    r = rec_dev.view(cnt, 20)
+    dt = r[:, 0:8].contiguous().view(torch.int64).view(-1)
+    i1 = r[:, 8:16].contiguous().view(torch.int64).view(-1)
+    sim = r[:, 16:20].contiguous().view(torch.int32).view(-1)
+    key = dt * (1 << 32) + i1
+    assert bool(torch.all(key[1:] > key[:-1]).item())
+    assert int(dt.min().item()) >= 1 and int((i1 + dt).max().item()) < n
+    assert int(sim.min().item()) >= m
+    for a in range(0, cnt, 1 << 20):
+        b = min(cnt, a + (1 << 20))
+        ka = rkeys.index_select(0, i1[a:b])
+        kb = rkeys.index_select(0, i1[a:b] + dt[a:b])
+        assert torch.equal((ka == kb).sum(1).to(torch.int32), sim[a:b])
+
+
+def test_cfg1_full_scale_properties(ls):
+    """BASELINE cfg1 at full size (N = 8e6) with the filter, and N = 2e6
+    without: properties checked on the GPU (the oracle cannot run there)."""
+    import torch
+    from paper_1803_09835_b200 import minmax_hash as mh
+    from paper_1803_09835_b200 import workloads
+    mapping = mh.gen_hash_mapping(4096, 100, 4, 0)
+    for n, occ in [(8_000_000, 1.5e-5), (2_000_000, None)]:
+        bits, _ = workloads.cfg1_bits_torch(n=n, seed=11, device=torch.device("cuda"))
+        keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
+        del bits
+        cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, occurrence_threshold=occ)
+        trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0)
+        _check_triplets_against_keys(trip, rkeys, n, 5)
+        assert st.emitted_triplets == trip.numel() // 20
+        if occ is None:
+            bs = ds.bsize[: ds.nb].to(torch.int64)
+            assert st.lookups_total == int((bs * (bs - 1)).sum().item())
+            assert st.distinct_pairs <= st.lookups_total // 2
+            assert st.n_queries == n and st.filtered_fingerprints == 0
+        else:
+            assert 0 < st.filtered_fingerprints < n
+        del keys, rkeys, tags, trip, ds
+        torch.cuda.empty_cache()
