@@ -368,6 +368,17 @@ def run_ours(args):
                          " tables" if tables_mode else "")),
             "algorithmic_bytes": pair_bytes, "hits": hits, "passes": passes,
             "ms": pair_ms}
+    # the other stages against the same accounting, for transparency
+    kt = len(ds.table_ids) if ds.table_ids is not None else 100
+    stage_roofs = {}
+    for name, nbytes in [("buckets", 12 * n * kt), ("minhash" + ("+gather" if tables_mode else ""),
+                                                     (4 * 400 + 8 * 100) * (n if not tables_mode
+                                                                            else -(-n // world)))]:
+        if stages.get(name):
+            gbs = nbytes / (stages[name] / 1e3) / 1e9
+            stage_roofs[name] = {"algorithmic_bytes": nbytes, "ms": stages[name],
+                                 "achieved_gbs": gbs, "frac": gbs / hbm}
+    roof["other_stages"] = stage_roofs
 
     e2e = None
     if not args.no_e2e:
