@@ -691,7 +691,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
             };
             uint32_t u = bbeg;
             const uint32_t* R = rows + bbeg * C::ROWP;
-            if (MODE == MODE_MATCHED) {
+#ifndef QS_UNROLL_M
+#define QS_UNROLL_M 0
+#endif
+            if (MODE == MODE_MATCHED && QS_UNROLL_M) {
                 // two B rows per step: independent LOP3 chains overlap their latencies
                 for (; u + 1 < bend; u += 2, R += 2 * C::ROWP) {
                     bool s0, s1;
