@@ -120,6 +120,22 @@ int qs_lsh_list_buckets(const uint64_t* skeys_dev, uint64_t n, uint32_t t,
                         const uint32_t* table_ids_dev, uint64_t* counts_dev, void* ws_dev,
                         size_t ws_bytes, void* stream);
 
+/* Bucket construction for the search: the member ids of qs_lsh_build_buckets
+ * in ids_out_dev (t, n) uint32, plus flags_out_dev (t, n) uint8 — bit 0:
+ * first member of its bucket, bit 1: last member — in place of the sorted-key
+ * array (the caller never sees it; it lives in the workspace). */
+size_t qs_lsh_bucket_flags_ws_bytes(uint64_t n, uint32_t t);
+int qs_lsh_build_bucket_flags(const uint64_t* keys_dev, uint64_t n, uint32_t t,
+                              uint32_t* ids_out_dev, uint8_t* flags_out_dev,
+                              void* ws_dev, size_t ws_bytes, void* stream);
+
+/* qs_lsh_list_buckets over the flag bytes of qs_lsh_build_bucket_flags. */
+size_t qs_lsh_list_flags_ws_bytes(uint64_t n, uint32_t t);
+int qs_lsh_list_buckets_flags(const uint8_t* flags_dev, uint64_t n, uint32_t t,
+                              uint64_t* bstart_dev, uint32_t* bsize_dev, uint32_t* btab_dev,
+                              const uint32_t* table_ids_dev, uint64_t* counts_dev,
+                              void* ws_dev, size_t ws_bytes, void* stream);
+
 /* SearchStats bucket fields (lsh_search.py:70-109, 295-302): lookups_total
  * (counted before the canonical/dt/exclusion masks, :192-194), the sizes of
  * the per-partition-table buckets (histogram of sizes < hist_len into

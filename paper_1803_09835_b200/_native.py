@@ -43,6 +43,10 @@ SIGNATURES = {
     "qs_lsh_build_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _sz, _p]),
     "qs_lsh_list_ws_bytes": (_sz, [_u64, _u32]),
     "qs_lsh_list_buckets": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _p, _p, _sz, _p]),
+    "qs_lsh_bucket_flags_ws_bytes": (_sz, [_u64, _u32]),
+    "qs_lsh_build_bucket_flags": (_int, [_p, _u64, _u32, _p, _p, _p, _sz, _p]),
+    "qs_lsh_list_flags_ws_bytes": (_sz, [_u64, _u32]),
+    "qs_lsh_list_buckets_flags": (_int, [_p, _u64, _u32, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "qs_lsh_bucket_stats": (_int, [_p, _p, _p, _u64, _p, _p, _u32, _p, _u32, _p, _u64, _p, _p]),
     "qs_lsh_compact_ws_bytes": (_sz, [_u64]),
     "qs_lsh_compact_buckets": (_int, [_p, _p, _p, _p, _u64, _p, _p, _p, _p, _p, _p,

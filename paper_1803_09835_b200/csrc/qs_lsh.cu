@@ -498,6 +498,13 @@ __global__ void k_make_sizes(const uint64_t* __restrict__ heads, const uint64_t*
     }
 }
 
+int make_bucket_sizes(const uint64_t* bstart, const uint64_t* counts, uint64_t n, uint32_t* bsize,
+                      uint32_t* btab, const uint32_t* table_ids, cudaStream_t st) {
+    k_make_sizes<<<148 * 8, 256, 0, st>>>(bstart, counts, n, bsize, btab, table_ids);
+    QS_CHECK_LAUNCH("bucket sizes");
+    return QS_OK;
+}
+
 // ----------------------------------------------------------------- stats
 constexpr int ST_HIST = 256;
 

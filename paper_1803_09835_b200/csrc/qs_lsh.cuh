@@ -18,6 +18,8 @@ int scan_u64(const uint64_t* in, uint64_t* out, uint64_t len, uint64_t* total, v
              cudaStream_t st);
 size_t scan_ws_bytes(uint64_t len);
 int num_sms();
+int make_bucket_sizes(const uint64_t* bstart, const uint64_t* counts, uint64_t n, uint32_t* bsize,
+                      uint32_t* btab, const uint32_t* table_ids, cudaStream_t st);
 
 __device__ __forceinline__ uint64_t mix_key(uint64_t s) { return fmix64(s ^ GOLDEN64); }
 

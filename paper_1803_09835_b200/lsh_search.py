@@ -186,17 +186,17 @@ class DeviceSearch:
         torch, n, t = self.torch, self.n, self.kt
         lib = nat.lib()
         self._mark("buckets")
-        skeys = torch.empty((t, n), dtype=torch.int64, device=self.dev)
         self.sids = torch.empty((t, n), dtype=torch.int32, device=self.dev)
-        ws = self._empty(lib.qs_lsh_bucket_ws_bytes(n, t))
-        nat.call("qs_lsh_build_buckets", nat.ptr(self.keys), n, t, nat.ptr(skeys),
-                 nat.ptr(self.sids), nat.ptr(ws), ws.numel(), nat.stream())
+        flags = torch.empty((t, n), dtype=torch.uint8, device=self.dev)
+        ws = self._empty(lib.qs_lsh_bucket_flags_ws_bytes(n, t))
+        nat.call("qs_lsh_build_bucket_flags", nat.ptr(self.keys), n, t, nat.ptr(self.sids),
+                 nat.ptr(flags), nat.ptr(ws), ws.numel(), nat.stream())
         del ws
-        self.launches += 3 * 3 + 3
+        self.launches += 3 * 3 + 5
         self._mark("list")
-        lws = self._empty(lib.qs_lsh_list_ws_bytes(n, t))
+        lws = self._empty(lib.qs_lsh_list_flags_ws_bytes(n, t))
         counts = torch.zeros(2, dtype=torch.int64, device=self.dev)
-        nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, None, None, None, None,
+        nat.call("qs_lsh_list_buckets_flags", nat.ptr(flags), n, t, None, None, None, None,
                  nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
         nb, heads = (int(v) for v in counts.tolist())
         self.nb, self.heads = nb, heads
@@ -204,10 +204,10 @@ class DeviceSearch:
         self.bsize = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         self.btab = torch.empty(max(nb, 1), dtype=torch.int32, device=self.dev)
         if nb:
-            nat.call("qs_lsh_list_buckets", nat.ptr(skeys), n, t, nat.ptr(self.bstart),
+            nat.call("qs_lsh_list_buckets_flags", nat.ptr(flags), n, t, nat.ptr(self.bstart),
                      nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(self.table_ids),
                      nat.ptr(counts), nat.ptr(lws), lws.numel(), nat.stream())
-        self.launches += 7 + 9
+        self.launches += 7 + 8
         self.full = (self.sids, self.bstart, self.bsize, self.btab, self.nb)
 
     def compact(self, emask):
