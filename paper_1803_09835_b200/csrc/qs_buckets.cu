@@ -16,15 +16,17 @@
 
 namespace qs {
 
-// radix-path result -> flags (adjacent key comparisons)
-__global__ void k_flags_from_keys(const uint64_t* __restrict__ sk, uint64_t n, uint64_t total,
+// sorted keys -> flags (adjacent key comparisons); grid (blocks, t)
+__global__ void k_flags_from_keys(const uint64_t* __restrict__ sk, uint64_t n,
                                   uint8_t* __restrict__ flags) {
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t pos = g % n, key = sk[g];
-        const bool head = pos == 0 || sk[g - 1] != key;
-        const bool tail = pos == n - 1 || sk[g + 1] != key;
-        flags[g] = (uint8_t)((head ? 1 : 0) | (tail ? 2 : 0));
+    const uint64_t* k = sk + (uint64_t)blockIdx.y * n;
+    uint8_t* f = flags + (uint64_t)blockIdx.y * n;
+    for (uint64_t pos = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pos < n;
+         pos += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = k[pos];
+        const bool head = pos == 0 || k[pos - 1] != key;
+        const bool tail = pos == n - 1 || k[pos + 1] != key;
+        f[pos] = (uint8_t)((head ? 1 : 0) | (tail ? 2 : 0));
     }
 }
 
@@ -153,7 +155,7 @@ int qs_lsh_build_bucket_flags(const uint64_t* keys_dev, uint64_t n, uint32_t t,
     int rc = qs_lsh_build_buckets(keys_dev, n, t, skeys, ids_out_dev, rws,
                                   qs_lsh_bucket_ws_bytes(n, t), stream);
     if (rc) return rc;
-    k_flags_from_keys<<<qs_blocks(total, 256), 256, 0, st>>>(skeys, n, total, flags_out_dev);
+    k_flags_from_keys<<<dim3(qs_blocks(n, 256, 1184), t), 256, 0, st>>>(skeys, n, flags_out_dev);
     QS_CHECK_LAUNCH("flags from keys");
     return QS_OK;
 }

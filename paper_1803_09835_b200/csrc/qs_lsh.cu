@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) k_prep(const uint64_t* __restrict__ sigs,
 // holding several distinct keys (prefix collisions) are then restored to
 // full-key order.  Detection reads the sorted keys once, coalesced; only the
 // first out-of-order position of a run reports the run start.
-constexpr uint32_t SORT_LO = 40;
+constexpr uint32_t SORT_LO = 32;
 
 constexpr uint32_t FIX_LMAX = 8192;   // elements sorted in shared memory per long run
 constexpr uint32_t FIX_LCAP = 65536;  // long runs listed per build
@@ -195,26 +195,28 @@ __device__ void insertion_run(uint64_t* __restrict__ keys, uint32_t* __restrict_
     }
 }
 
+// grid (blocks, t): table blockIdx.y, in-table positions grid-strided (no
+// 64-bit modulo per element)
 __global__ void k_fix_detect(const uint64_t* __restrict__ keys, uint64_t n, uint64_t total,
                              uint64_t* __restrict__ runs, uint64_t cap,
                              unsigned long long* __restrict__ nruns) {
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t pos = g % n;
-        if (pos == 0) continue;
-        const uint64_t k0 = keys[g], k1 = keys[g - 1];
+    (void)total;
+    const uint64_t* k = keys + (uint64_t)blockIdx.y * n;
+    for (uint64_t pos = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1; pos < n;
+         pos += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k0 = k[pos], k1 = k[pos - 1];
         if ((k0 >> SORT_LO) != (k1 >> SORT_LO) || k0 >= k1) continue;
-        // out of order at g: walk back to the run start; report only if no
+        // out of order at pos: walk back to the run start; report only if no
         // earlier out-of-order position in the run
-        uint64_t j = g - 1;
+        uint64_t j = pos - 1;
         bool firstbad = true;
-        while (j > g - pos && (keys[j - 1] >> SORT_LO) == (k0 >> SORT_LO)) {
-            if (keys[j] < keys[j - 1]) firstbad = false;
+        while (j > 0 && (k[j - 1] >> SORT_LO) == (k0 >> SORT_LO)) {
+            if (k[j] < k[j - 1]) firstbad = false;
             --j;
         }
         if (!firstbad) continue;
         const unsigned long long o = atomicAdd(nruns, 1ULL);
-        if (o < cap) runs[o] = j;
+        if (o < cap) runs[o] = (uint64_t)blockIdx.y * n + j;
     }
 }
 
@@ -802,7 +804,8 @@ int qs_lsh_build_buckets(const uint64_t* keys_dev, uint64_t n, uint32_t t, uint6
     if (rc) return rc;
     QS_CUDA(cudaMemsetAsync(nruns, 0, 16, st), "memset");
     const unsigned g = qs_blocks(total, 256);
-    k_fix_detect<<<g, 256, 0, st>>>(keys_out_dev, n, total, runs, cap, nruns);
+    k_fix_detect<<<dim3(qs_blocks(n, 256, 1184), t), 256, 0, st>>>(keys_out_dev, n, total, runs,
+                                                                    cap, nruns);
     k_fix_runs<<<148 * 16, 256, 0, st>>>(keys_out_dev, ids_out_dev, n, runs, cap, nruns, longruns);
     const int long_smem = (int)(FIX_LMAX * 16);
     QS_CUDA(cudaFuncSetAttribute(k_fix_long_runs, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(RSC_T) k_rs_scan_down(uint32_t* __restrict__ a
 // Stable scatter of one tile: rank in input order per digit, stage the tile in
 // shared memory in (digit, input) order, then write each digit's run to its
 // global slot with consecutive threads on consecutive addresses (coalesced).
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
+__global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(
     const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t seg_len,
     uint32_t tiles, uint32_t shift, const uint32_t* __restrict__ offs,
     uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals) {
@@ -196,12 +196,18 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
     uint32_t v[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
     const uint32_t lt = (1u << lane) - 1u;
+    // all loads in flight before the ranking (its warp syncs would serialise them)
 #pragma unroll
     for (int r = 0; r < RS_ITEMS; ++r) {
         const uint64_t i = t0 + (uint64_t)r * 32 + lane;
         const bool ok = i < seg_len;
-        k[r] = ok ? keys[base + i] : 0;
-        v[r] = ok ? (vals ? vals[base + i] : (uint32_t)i) : 0;  // no vals: in-segment position
+        k[r] = ok ? __ldcs(keys + base + i) : 0;
+        v[r] = ok ? (vals ? __ldcs(vals + base + i) : (uint32_t)i) : 0;  // no vals: position
+    }
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+        const uint64_t i = t0 + (uint64_t)r * 32 + lane;
+        const bool ok = i < seg_len;
         const uint32_t dgt = ok ? (uint32_t)((k[r] >> shift) & 0xFF) : 0x100u;
 #ifndef QS_RS_MATCH
         uint32_t peers = 0xffffffffu;  // lanes with the same digit, from 9 ballots
