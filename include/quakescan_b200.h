@@ -77,6 +77,16 @@ int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K
                                 uint64_t* rkeys_dev, uint32_t* tags_dev, uint32_t* bad_dev,
                                 void* stream);
 
+/* The same for rows [row0, row0 + nrows) of the n-row layout (bits_dev,
+ * keys_dev, rkeys_dev, tags_dev and sigs_dev all address the full n rows):
+ * lets a caller overlap the signatures of landed rows with the host->device
+ * copy of later ones. */
+int qs_minmax_signatures_search_rows(const uint32_t* bits_dev, uint64_t n, uint64_t row0,
+                                     uint64_t nrows, uint32_t K, const void* plan_dev,
+                                     uint32_t d, uint32_t t, uint32_t k_half, uint64_t* sigs_dev,
+                                     uint64_t* keys_dev, uint64_t* rkeys_dev, uint32_t* tags_dev,
+                                     uint32_t* bad_dev, void* stream);
+
 /* HOST-buffer drop-in for the reference's native plugin point
  * `_core.gen_signatures_range(bits, values, t, k_half, out, start, stop)`
  * (minmax_hash.py:24-30 selects it; _sigcore.pyx:32-36 defines it): fills

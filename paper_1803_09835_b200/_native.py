@@ -36,6 +36,8 @@ SIGNATURES = {
     "qs_minmax_signatures": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p]),
     "qs_minmax_signatures_search": (_int, [_p, _u64, _u32, _p, _u32, _u32, _u32, _p, _p, _p,
                                            _p, _p, _p]),
+    "qs_minmax_signatures_search_rows": (_int, [_p, _u64, _u64, _u64, _u32, _p, _u32, _u32, _u32,
+                                                _p, _p, _p, _p, _p, _p]),
     "qs_gen_signatures_range": (_int, [_p, _u64, _u32, _p, _u32, _u32, _i32, _i32, _p, _u64,
                                        _u64]),
     "qs_lsh_prep": (_int, [_p, _u64, _u32, _p, _p, _p, _p]),

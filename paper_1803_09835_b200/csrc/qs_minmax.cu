@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(256) k_signatures(
     const uint16_t* __restrict__ order, const uint64_t* __restrict__ svals, uint32_t d,
     uint32_t F, uint32_t t, uint32_t kh, uint64_t* __restrict__ sigs,
     uint64_t* __restrict__ keys, uint64_t* __restrict__ rkeys, uint32_t* __restrict__ tags,
-    uint32_t* __restrict__ bad) {
+    uint32_t* __restrict__ bad, uint64_t row0, uint64_t row_end) {
+    // rows [row0, row_end) of an n-row layout (n: the stride of keys / tags)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t words = (d + 31) >> 5;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(256) k_signatures(
     const uint32_t W = (t + 31) >> 5;
     const bool vec = (K % 4 == 0) && ((((uintptr_t)bits) & 15) == 0);
 
-    for (uint64_t row = gwarp; row < n; row += nwarps) {
+    for (uint64_t row = row0 + gwarp; row < row_end; row += nwarps) {
         for (uint32_t w = lane; w < words; w += 32) bm[w] = 0u;
         __syncwarp();
         const uint32_t* rb = bits + row * K;
@@ -217,11 +218,14 @@ static size_t sig_smem_per_warp(uint32_t d, uint32_t F) {
 static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
                              const void* plan, uint32_t d, uint32_t t, uint32_t kh,
                              uint64_t* sigs, uint64_t* keys, uint64_t* rkeys, uint32_t* tags,
-                             uint32_t* bad, cudaStream_t st) {
+                             uint32_t* bad, cudaStream_t st, uint64_t row0 = 0,
+                             uint64_t nrows = ~0ull) {
+    if (nrows == ~0ull) nrows = n - row0;
+    QS_ARG(row0 <= n && nrows <= n - row0, "row range out of bounds");
     QS_ARG(K >= 1, "fingerprints must have at least one set bit");
     QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
     QS_ARG(t >= 1 && kh >= 1, "t and k/2 must be >= 1");
-    if (n == 0) return QS_OK;
+    if (nrows == 0) return QS_OK;
     const uint32_t F = t * kh;
     const uint16_t* order = (const uint16_t*)plan;
     const uint64_t* svals = (const uint64_t*)((const unsigned char*)plan + plan_order_bytes(d, F));
@@ -231,7 +235,7 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     QS_ARG(per_warp <= 220 * 1024, "t*k too large for the signature kernel (F=%u)", F);
     size_t smem = per_warp * warps;
     unsigned threads = warps * 32;
-    uint64_t want = (n + warps - 1) / warps;
+    uint64_t want = (nrows + warps - 1) / warps;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -247,10 +251,12 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     unsigned grid = (unsigned)(want < cap ? want : cap);
     if (search)
         k_signatures<true><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
-                                                         sigs, keys, rkeys, tags, bad);
+                                                         sigs, keys, rkeys, tags, bad, row0,
+                                                         row0 + nrows);
     else
         k_signatures<false><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
-                                                          sigs, nullptr, nullptr, nullptr, bad);
+                                                          sigs, nullptr, nullptr, nullptr, bad,
+                                                          row0, row0 + nrows);
     QS_CHECK_LAUNCH("k_signatures");
     return QS_OK;
 }
@@ -305,6 +311,15 @@ int qs_minmax_signatures_search(const uint32_t* bits_dev, uint64_t n, uint32_t K
                                 uint32_t* tags_dev, uint32_t* bad_dev, void* stream) {
     return launch_signatures(true, bits_dev, n, K, plan_dev, d, t, k_half, sigs_dev, keys_dev,
                              rkeys_dev, tags_dev, bad_dev, (cudaStream_t)stream);
+}
+
+int qs_minmax_signatures_search_rows(const uint32_t* bits_dev, uint64_t n, uint64_t row0,
+                                     uint64_t nrows, uint32_t K, const void* plan_dev, uint32_t d,
+                                     uint32_t t, uint32_t k_half, uint64_t* sigs_dev,
+                                     uint64_t* keys_dev, uint64_t* rkeys_dev, uint32_t* tags_dev,
+                                     uint32_t* bad_dev, void* stream) {
+    return launch_signatures(true, bits_dev, n, K, plan_dev, d, t, k_half, sigs_dev, keys_dev,
+                             rkeys_dev, tags_dev, bad_dev, (cudaStream_t)stream, row0, nrows);
 }
 
 int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,

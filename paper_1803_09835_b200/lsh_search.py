@@ -528,21 +528,72 @@ def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
     return out
 
 
+def _search_layout(n: int, t: int, device, with_keys: bool = True):
+    torch = nat.torch()
+    W = (t + 31) // 32
+    keys = torch.empty((t, n), dtype=torch.int64, device=device) if with_keys else None
+    rkeys = torch.empty((n, t), dtype=torch.int64, device=device)
+    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=device)
+    bad = torch.zeros(1, dtype=torch.int32, device=device)
+    return keys, rkeys, tags, bad
+
+
 def signatures_for_search(bits, mapping: HashMapping, with_keys: bool = True):
     """Fused Min-Max kernel writing table-major keys + tags directly (no
     row-major signature round trip). bits: CUDA int32 (n, K)."""
-    torch = nat.torch()
     n, K = bits.shape
     t = mapping.t
-    W = (t + 31) // 32
     _, plan = mapping.device_plan()
-    keys = torch.empty((t, n), dtype=torch.int64, device=bits.device) if with_keys else None
-    rkeys = torch.empty((n, t), dtype=torch.int64, device=bits.device)
-    tags = torch.empty((2, n, W, 8), dtype=torch.int32, device=bits.device)
-    bad = torch.zeros(1, dtype=torch.int32, device=bits.device)
+    keys, rkeys, tags, bad = _search_layout(n, t, bits.device, with_keys)
     nat.call("qs_minmax_signatures_search", nat.ptr(bits), n, K, nat.ptr(plan), mapping.d, t,
              mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags), nat.ptr(bad),
              nat.stream())
+    return keys, rkeys, tags, bad
+
+
+def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_bytes: int = 256 << 20):
+    """Host (n, K) int32 bits -> the search layout, the host->device copy
+    pipelined with the signature kernel: row chunks go through two pinned
+    staging buffers on a copy stream (the host copy into one buffer split over
+    a thread pool while the other's DMA runs) and the kernel signs each chunk's
+    rows (qs_minmax_signatures_search_rows) on the compute stream as soon as
+    they land."""
+    torch = nat.torch()
+    n, K = arr.shape
+    t = mapping.t
+    _, plan = mapping.device_plan()
+    keys, rkeys, tags, bad = _search_layout(n, t, "cuda")
+    bdev = torch.empty((n, K), dtype=torch.int32, device="cuda")
+    if n == 0:
+        return keys, rkeys, tags, bad
+    rows_per = max(1, chunk_bytes // (K * 4))
+    stage = [torch.empty((min(rows_per, n), K), dtype=torch.int32).pin_memory() for _ in range(2)]
+    done = [None, None]
+    pool = _copy_pool()
+    nthr = pool._max_workers
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    copy.wait_stream(compute)  # bdev's allocation is ordered on the compute stream
+    for k, r0 in enumerate(range(0, n, rows_per)):
+        r1 = min(n, r0 + rows_per)
+        sl = k & 1
+        if done[sl] is not None:
+            done[sl].synchronize()
+        host = stage[sl].numpy()
+        rows = r1 - r0
+        step = max(1, (1 << 18) // K, -(-rows // nthr))
+        list(pool.map(lambda i: np.copyto(host[i:min(rows, i + step)], arr[r0 + i:r0 + min(rows, i + step)]),
+                      range(0, rows, step)))
+        with torch.cuda.stream(copy):
+            bdev[r0:r1].copy_(stage[sl][:rows], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        done[sl] = ev
+        compute.wait_event(ev)
+        nat.call("qs_minmax_signatures_search_rows", nat.ptr(bdev), n, r0, rows, K, nat.ptr(plan),
+                 mapping.d, t, mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
+                 nat.ptr(bad), nat.stream())
+    bdev.record_stream(copy)
     return keys, rkeys, tags, bad
 
 
@@ -570,10 +621,7 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
             raise ParameterError("bits must be a 2-D (n, K) array")
         if arr.shape[1] < 1:
             raise ParameterError("fingerprints must have at least one set bit")
-        # the range check (minmax_hash.py:107-108) runs on the device, flagged by
-        # the signature kernel, instead of a host pass over the whole array
-        bdev = _to_device_staged(arr.view(np.int32))
-    n, K = bdev.shape
+    n, K = bdev.shape if on_device else arr.shape
     if K < 1:
         raise ParameterError("fingerprints must have at least one set bit")
     if n >= 2**32:
@@ -582,7 +630,12 @@ def search_fingerprints(fps, cfg: SearchConfig, mapping: HashMapping | None = No
     if n == 0:
         empty = _empty_triplets() if not on_device else torch.empty(0, dtype=torch.uint8, device="cuda")
         return empty, SearchStats(n_fingerprints=0), mapping
-    keys, rkeys, tags, bad = signatures_for_search(bdev, mapping)
+    if on_device:
+        keys, rkeys, tags, bad = signatures_for_search(bdev, mapping)
+    else:
+        # the range check (minmax_hash.py:107-108) runs on the device, flagged by
+        # the signature kernel, instead of a host pass over the whole array
+        keys, rkeys, tags, bad = signatures_for_search_host(arr.view(np.int32), mapping)
     if int(bad.item()):
         raise ParameterError("fingerprint bit index out of range for mapping")
     trip, stats, _ = run_search(keys, rkeys, tags, n, cfg.tables, cfg, excl)

@@ -120,3 +120,23 @@ def test_errors(mh):
     with pytest.raises(ParameterError):
         mh.gen_hash_mapping(8, 1, 3, 0)
     assert mh.signatures(np.zeros((0, 5), np.uint32), m).shape == (0, 2)
+
+
+def test_host_pipelined_search_layout_matches_device(mh):
+    """search_fingerprints' host path (row chunks staged and signed as they
+    land, qs_minmax_signatures_search_rows) == the device-resident path."""
+    import torch
+    from paper_1803_09835_b200 import lsh_search as ls
+    from paper_1803_09835_b200 import workloads
+    bits, _ = workloads.cfg1_bits(n=5000, seed=3, pair_frac=1 / 50, group_frac=1 / 1000)
+    m = mh.gen_hash_mapping(4096, 100, 4, 0)
+    arr = np.ascontiguousarray(bits, dtype=np.uint32).view(np.int32)
+    want = ls.signatures_for_search(torch.from_numpy(arr).cuda(), m)
+    got = ls.signatures_for_search_host(arr, m, chunk_bytes=1777 * bits.shape[1] * 4)  # 3 ragged chunks
+    torch.cuda.synchronize()
+    for g, w in zip(got, want):
+        assert torch.equal(g, w)
+    bad = arr.copy()
+    bad[4321, 7] = 4096
+    got = ls.signatures_for_search_host(bad, m, chunk_bytes=1000 * bits.shape[1] * 4)
+    assert int(got[3].item()) == 1
