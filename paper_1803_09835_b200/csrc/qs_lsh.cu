@@ -509,6 +509,7 @@ int make_bucket_sizes(const uint64_t* bstart, const uint64_t* counts, uint64_t n
 
 // ----------------------------------------------------------------- stats
 constexpr int ST_HIST = 256;
+constexpr uint32_t KEEP_LANE = 16;  // compaction: buckets above this are handled by a warp
 
 __device__ __forceinline__ void stats_piece(uint64_t nP, unsigned long long* sh,
                                             unsigned long long* __restrict__ hist,
@@ -603,12 +604,37 @@ __global__ void __launch_bounds__(256) k_keep_count(
         __syncthreads();
     }
     unsigned long long looks = 0, pieces = 0, mx = 0;
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
-         b += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t st = bstart[b];
-        const uint32_t s = bsize[b];
+    const uint32_t lane = threadIdx.x & 31;
+    // a warp takes 32 consecutive buckets: a lane counts its own bucket when it
+    // is small; buckets above KEEP_LANE members are counted by the whole warp
+    // afterwards (coalesced member reads, no single-lane tail)
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t b0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; b0 < nb;
+         b0 += nwarps * 32) {
+        const uint64_t b = b0 + lane;
+        uint64_t st = 0;
+        uint32_t s = 0;
+        if (b < nb) {
+            st = bstart[b];
+            s = bsize[b];
+        }
         uint32_t k = 0;
-        for (uint32_t j = 0; j < s; ++j) k += ex[sids[st + j]] == 0;
+        const bool lone = s <= KEEP_LANE;
+        if (lone)
+            for (uint32_t j = 0; j < s; ++j) k += ex[sids[st + j]] == 0;
+        uint32_t bigl = __ballot_sync(0xffffffffu, !lone);
+        while (bigl) {
+            const int src = __ffs(bigl) - 1;
+            bigl &= bigl - 1;
+            const uint64_t bst = __shfl_sync(0xffffffffu, st, src);
+            const uint32_t bs = __shfl_sync(0xffffffffu, s, src);
+            uint32_t kk = 0;
+            for (uint32_t j = lane; j < bs; j += 32) kk += ex[sids[bst + j]] == 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
+            if (lane == (uint32_t)src) k = kk;
+        }
+        if (b >= nb) continue;
         cnt[b] = k >= 2 ? k : 0;
         flag[b] = k >= 2 ? 1 : 0;
         if (hist) {
@@ -642,20 +668,51 @@ __global__ void k_keep_write(const uint32_t* __restrict__ sids, const uint64_t* 
                              const uint64_t* __restrict__ slot, uint32_t* __restrict__ sids2,
                              uint64_t* __restrict__ bstart2, uint32_t* __restrict__ bsize2,
                              uint32_t* __restrict__ btab2) {
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
-         b += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = cnt_raw[b];
-        if (!k) continue;
-        const uint64_t st = bstart[b], o = mem_off[b], sl = slot[b];
-        const uint32_t s = bsize[b];
-        uint64_t w = o;
-        for (uint32_t j = 0; j < s; ++j) {
-            const uint32_t x = sids[st + j];
-            if (!ex[x]) sids2[w++] = x;
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t b0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; b0 < nb;
+         b0 += nwarps * 32) {
+        const uint64_t b = b0 + lane;
+        const uint64_t k = b < nb ? cnt_raw[b] : 0;
+        uint64_t st = 0, o = 0;
+        uint32_t s = 0;
+        if (k) {
+            st = bstart[b];
+            o = mem_off[b];
+            s = bsize[b];
+            const uint64_t sl = slot[b];
+            bstart2[sl] = o;
+            bsize2[sl] = (uint32_t)k;
+            btab2[sl] = btab[b];
         }
-        bstart2[sl] = o;
-        bsize2[sl] = (uint32_t)k;
-        btab2[sl] = btab[b];
+        const bool lone = s <= KEEP_LANE;
+        if (k && lone) {
+            uint64_t w = o;
+            for (uint32_t j = 0; j < s; ++j) {
+                const uint32_t x = sids[st + j];
+                if (!ex[x]) sids2[w++] = x;
+            }
+        }
+        uint32_t bigl = __ballot_sync(0xffffffffu, k && !lone);
+        while (bigl) {
+            const int src = __ffs(bigl) - 1;
+            bigl &= bigl - 1;
+            const uint64_t bst = __shfl_sync(0xffffffffu, st, src);
+            const uint32_t bs = __shfl_sync(0xffffffffu, s, src);
+            uint64_t w = __shfl_sync(0xffffffffu, o, src);
+            for (uint32_t j0 = 0; j0 < bs; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                uint32_t x = 0;
+                bool keep = false;
+                if (j < bs) {
+                    x = sids[bst + j];
+                    keep = !ex[x];
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) sids2[w + __popc(bal & lt)] = x;
+                w += __popc(bal);
+            }
+        }
     }
 }
 
