@@ -375,9 +375,19 @@ def run_ours(args):
                                                      (4 * 400 + 8 * 100) * (n if not tables_mode
                                                                             else -(-n // world)))]:
         if stages.get(name):
-            gbs = nbytes / (stages[name] / 1e3) / 1e9
-            stage_roofs[name] = {"algorithmic_bytes": nbytes, "ms": stages[name],
+            sms = stages[name] + (stages.get("list", 0.0) if name == "buckets" else 0.0)
+            gbs = nbytes / (sms / 1e3) / 1e9
+            stage_roofs[name] = {"algorithmic_bytes": nbytes, "ms": sms,
                                  "achieved_gbs": gbs, "frac": gbs / hbm}
+            if name == "buckets":
+                # bytes the build really moves per (fp, table): 4 radix histogram
+                # reads (4 x 8) + scatter passes (8 + 12 | 3 x (12 + 12)) + flag
+                # sweep (8 + 1) + listing (~2): DESIGN.md section 5.2
+                moved = 143 * n * kt
+                stage_roofs[name].update({"scope": "bucket build + listing",
+                                          "moved_bytes": moved,
+                                          "moved_gbs": moved / (sms / 1e3) / 1e9,
+                                          "moved_frac": moved / (sms / 1e3) / 1e9 / hbm})
     roof["other_stages"] = stage_roofs
 
     e2e = None
