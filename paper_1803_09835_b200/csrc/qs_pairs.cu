@@ -91,27 +91,33 @@ __device__ unsigned long long g_prof[8];
 
 // Staged row layout of a launch: tag planes kept per 32-table word.  MATCHED
 // screens with planes 0-7 of every word; DISTINCT (one launch per table word
-// WT, W = WT + 1) needs all 16 planes of words <= WT; FULL (one launch per
-// word WT) needs 16 planes of words <= WT (first-table test) and 8 of the
-// later words (count screen).
+// WT, W = WT + 1) screens the words <= WT with planes 0-11 (a false early
+// match, 1/4096 per table, only queues the pair for key confirmation); FULL
+// (one launch per word WT) needs 16 planes of words <= WT (first-table test)
+// and 8 of the later words (count screen).
+constexpr int DISTINCT_PLANES = 12;
 template <int MODE, int WT>
 struct Layout {
     static constexpr int planes(int w) {
-        return MODE == MODE_MATCHED ? 8 : (MODE == MODE_DISTINCT ? 16 : (w <= WT ? 16 : 8));
+        return MODE == MODE_MATCHED ? 8
+             : (MODE == MODE_DISTINCT ? DISTINCT_PLANES : (w <= WT ? 16 : 8));
     }
     static constexpr int off(int w) {  // closed form: folds to an immediate in unrolled loops
         return MODE == MODE_MATCHED ? 8 * w
-             : (MODE == MODE_DISTINCT || w <= WT + 1 ? 16 * w : 16 * (WT + 1) + 8 * (w - WT - 1));
+             : (MODE == MODE_DISTINCT ? DISTINCT_PLANES * w
+                : (w <= WT + 1 ? 16 * w : 16 * (WT + 1) + 8 * (w - WT - 1)));
     }
 };
 
 template <int W, int MODE, int WT>
 struct TileCfg {
     using Lay = Layout<MODE, WT>;
-    static constexpr int NP = MODE == MODE_MATCHED ? 8 : 16;  // max planes per word (registers)
+    static constexpr int NP = MODE == MODE_MATCHED ? 8
+                            : (MODE == MODE_DISTINCT ? DISTINCT_PLANES : 16);  // planes in registers
     static constexpr int ROW = Lay::off(W);                   // u32 per staged row
-    static constexpr int ROWP = ROW + 4;                      // padded stride: row-parallel
-                                                              // 16-byte loads are conflict-free
+    // padded stride, an odd number of 16-byte units: row-parallel 16-byte
+    // loads are conflict-free
+    static constexpr int ROWP = ((ROW + 4) / 4) % 2 ? ROW + 4 : ROW + 8;
     // DISTINCT launches per table word with only words <= that word staged:
     // narrow rows (W <= 2) run more CTAs with smaller buffers
     static constexpr int BUFKB = MODE == MODE_MATCHED ? QS_BUFKB_M
@@ -631,7 +637,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     for (int w = 0; w < W; ++w) {
                         uint32_t x = 0;
                         if (w <= WT) {  // launches are per table word: wt == WT
-                            x = pmask<W, NP>(A, R, w, 16, Lay::off(w));
+                            x = pmask<W, NP>(A, R, w, Lay::planes(w), Lay::off(w));
                             if (w == (int)wg - 1) x &= last_mask;
                             early |= (w < WT) ? x : (x & low);
                             if (w == WT) cnt += __popc(x & ~low);
