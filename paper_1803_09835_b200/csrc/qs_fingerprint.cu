@@ -147,19 +147,37 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
             if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 0xFF], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const uint32_t need = *s_krem;
-            uint32_t cum = 0;
-            int dsel = 0;
-            for (int dgt = 255; dgt >= 0; --dgt) {
-                if (cum + hist[dgt] >= need) {
-                    dsel = dgt;
-                    break;
-                }
-                cum += hist[dgt];
+        if (threadIdx.x < 32) {
+            // warp 0 finds the digit holding the need-th largest key: lane l owns
+            // bins [8l, 8l + 8); suffix sums over lanes, then one lane scans its bins
+            const uint32_t lane = threadIdx.x, need = *s_krem;
+            uint32_t c[8], sum = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                c[e] = hist[8 * lane + e];
+                sum += c[e];
             }
-            *s_krem = need - cum;
-            *s_prefix = prefix | ((uint64_t)dsel << shift);
+            uint32_t x = sum;  // sum over lanes >= lane
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
+                if (lane + o < 32) x += y;
+            }
+            const uint32_t above = x - sum;
+            if (above < need && need <= x) {
+                uint32_t cum = above;
+                int dsel = 8 * lane;
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    if (cum + c[e] >= need) {
+                        dsel = 8 * lane + e;
+                        break;
+                    }
+                    cum += c[e];
+                }
+                *s_krem = need - cum;
+                *s_prefix = prefix | ((uint64_t)dsel << shift);
+            }
         }
         pmask |= (uint64_t)0xFF << shift;
         __syncthreads();
