@@ -120,32 +120,39 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* wsum, u
 // largest |v'| among eligible coefficients with ties to the lower index, bit
 // 2j + (v' < 0), ascending.  `row` is overwritten with the scores.  Returns
 // false (and writes nothing) when a coefficient is not finite.
+// Radix select over keys[i] = |v'| bits + 1 (0: ineligible), 8 bits per pass
+// from the top; after each pass only the members matching the selected
+// prefix stay on a candidate list (la / lb, ping-pong), so the later passes
+// touch a handful of coefficients.  Scratch: keys u64[n], la / lb u16[n].
 __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med,
                          const double* __restrict__ mad, uint32_t top_k, uint32_t* __restrict__ ob,
-                         uint32_t* hist, uint32_t* wsum, uint64_t* s_prefix, uint32_t* s_krem) {
+                         uint32_t* hist, uint32_t* wsum, uint64_t* s_prefix, uint32_t* s_krem,
+                         uint64_t* keys, uint16_t* la, uint16_t* lb, uint32_t* s_cnt) {
     bool nonfinite = false;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double c = row[i];
         if (!isfinite(c)) nonfinite = true;
         const double md = mad[i];
-        row[i] = md > 0.0 ? (c - med[i]) / md : 0.0;
+        const double sc = md > 0.0 ? (c - med[i]) / md : 0.0;
+        row[i] = sc;
+        keys[i] = md > 0.0 ? mag_key(sc) + 1 : 0;
     }
-    if (__syncthreads_or(nonfinite)) return false;
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     if (threadIdx.x == 0) {
         *s_prefix = 0;
         *s_krem = top_k;
+        s_cnt[0] = 0;
     }
-    __syncthreads();
-    uint64_t pmask = 0;
+    if (__syncthreads_or(nonfinite)) return false;
+    // pass 0: histogram of the top byte over all eligible coefficients
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t k = keys[i];
+        if (k) atomicAdd(&hist[k >> 56], 1u);
+    }
+    uint16_t* cur = la;
+    uint16_t* nxt = lb;
+    uint32_t ncur = 0;
     for (int shift = 56; shift >= 0; shift -= 8) {
-        for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        const uint64_t prefix = *s_prefix;
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            if (!(mad[i] > 0.0)) continue;
-            const uint64_t k = mag_key(row[i]);
-            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 0xFF], 1u);
-        }
         __syncthreads();
         if (threadIdx.x < 32) {
             // warp 0 finds the digit holding the need-th largest key: lane l owns
@@ -176,20 +183,38 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
                     cum += c[e];
                 }
                 *s_krem = need - cum;
-                *s_prefix = prefix | ((uint64_t)dsel << shift);
+                *s_prefix |= (uint64_t)dsel << shift;
             }
         }
-        pmask |= (uint64_t)0xFF << shift;
         __syncthreads();
+        if (shift == 0) break;
+        // keep the members matching the selected digit, histogram their next digit
+        const uint32_t dsel = (uint32_t)(*s_prefix >> shift) & 0xFFu;
+        for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        if (threadIdx.x == 0) s_cnt[1] = 0;
+        __syncthreads();
+        const uint32_t lim = shift == 56 ? n : ncur;
+        for (uint32_t j = threadIdx.x; j < lim; j += blockDim.x) {
+            const uint32_t i = shift == 56 ? j : cur[j];
+            const uint64_t k = keys[i];
+            if (k && ((uint32_t)(k >> shift) & 0xFFu) == dsel) {
+                nxt[atomicAdd(&s_cnt[1], 1u)] = (uint16_t)i;
+                atomicAdd(&hist[(k >> (shift - 8)) & 0xFF], 1u);
+            }
+        }
+        __syncthreads();
+        ncur = s_cnt[1];
+        uint16_t* tsw = cur;
+        cur = nxt;
+        nxt = tsw;
     }
-    const uint64_t thr = *s_prefix;
+    const uint64_t thr = *s_prefix;  // key of the K-th largest (>= 1: eligible)
     // greater-than count and index-ordered ranks of ties (blocked ownership)
     const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
     const uint32_t i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
     uint32_t gt = 0, eq = 0;
     for (uint32_t i = i0; i < i1; ++i) {
-        if (!(mad[i] > 0.0)) continue;
-        const uint64_t k = mag_key(row[i]);
+        const uint64_t k = keys[i];
         gt += k > thr;
         eq += k == thr;
     }
@@ -199,8 +224,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     const uint32_t eq_before = block_scan_u32(eq, wsum, nullptr);
     uint32_t sel = 0, eqr = eq_before;
     for (uint32_t i = i0; i < i1; ++i) {
-        if (!(mad[i] > 0.0)) continue;
-        const uint64_t k = mag_key(row[i]);
+        const uint64_t k = keys[i];
         if (k > thr) ++sel;
         else if (k == thr) {
             if (eqr < need) ++sel;
@@ -210,15 +234,13 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     uint32_t pos = block_scan_u32(sel, wsum, nullptr);
     eqr = eq_before;
     for (uint32_t i = i0; i < i1; ++i) {
-        if (!(mad[i] > 0.0)) continue;
-        const double sc = row[i];
-        const uint64_t k = mag_key(sc);
+        const uint64_t k = keys[i];
         bool take = k > thr;
         if (k == thr) {
             take = eqr < need;
             ++eqr;
         }
-        if (take) ob[pos++] = 2 * i + (sc < 0.0 ? 1u : 0u);
+        if (take) ob[pos++] = 2 * i + (row[i] < 0.0 ? 1u : 0u);
     }
     return true;
 }
@@ -238,7 +260,9 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
     double* hs = img + n;                              // [F*T] Haar scratch
     double* tmp = hs + n;                              // [F*wmax]
     float* gs = (float*)(tmp + (uint64_t)F * g.wmax);  // [wmax*nb]
+    uint16_t* lists = (uint16_t*)(gs + (((uint64_t)g.wmax * nb + 3) & ~3ull));  // [2n] top-K candidates
     __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t wsum[32];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_krem;
@@ -325,7 +349,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
         }
         // ---- mode 3: scores, K-th largest |score| (radix select), bits
         if (!topk_row(img, n, med, mad, g.top_k, (uint32_t*)out + wi * g.top_k, hist, wsum,
-                      &s_prefix, &s_krem))
+                      &s_prefix, &s_krem, (uint64_t*)hs, lists, lists + n, s_cnt))
             if (threadIdx.x == 0) atomicOr(flags, 1u);
     }
 }
@@ -412,15 +436,19 @@ __global__ void __launch_bounds__(WIN_THREADS) k_topk_rows(const TC* __restrict_
                                                            uint32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* row = (double*)smem;
+    uint64_t* keys = (uint64_t*)(row + n);
+    uint16_t* lists = (uint16_t*)(keys + n);
     __shared__ uint32_t hist[256];
     __shared__ uint32_t wsum[32];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_krem;
+    __shared__ uint32_t s_cnt[2];
     for (uint64_t r = blockIdx.x; r < B; r += gridDim.x) {
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) row[i] = (double)c[r * n + i];
         __syncthreads();
-        if (!topk_row(row, n, med, mad, top_k, out + r * top_k, hist, wsum, &s_prefix, &s_krem))
+        if (!topk_row(row, n, med, mad, top_k, out + r * top_k, hist, wsum, &s_prefix, &s_krem,
+                      keys, lists, lists + n, s_cnt))
             if (threadIdx.x == 0) atomicOr(flags, 1u);
     }
 }
@@ -571,7 +599,8 @@ int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int
     QS_ARG(mode != 3 || (top_k >= 1 && top_k <= F * T), "bad top_k");
     if (n_win == 0) return QS_OK;
     (void)n_cols;
-    const size_t smem = (size_t)F * T * 16 + (size_t)F * wmax * 8 + (size_t)wmax * nb * 4 + 16;
+    const size_t smem = (size_t)F * T * 16 + (size_t)F * wmax * 8 +
+                        (((size_t)wmax * nb + 3) & ~(size_t)3) * 4 + (size_t)F * T * 4 + 16;
     QS_ARG(smem <= 200 * 1024, "spectral image too large for the window kernel");
     QS_CUDA(cudaFuncSetAttribute(k_windows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     WinGeom g{n_cols, lag, win, win0, n_win, frame, hop, nb, F, T, wmin, wmax, n_levels, top_k,
@@ -609,7 +638,7 @@ int qs_fp_topk_bits(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
                     uint32_t* flags_dev, void* stream) {
     QS_ARG(top_k >= 1 && top_k <= n, "top_k must be in [1, n]");
     if (B == 0) return QS_OK;
-    const size_t smem = (size_t)n * 8;
+    const size_t smem = (size_t)n * 20;  // row f64 + keys u64 + two u16 candidate lists
     QS_ARG(smem <= 200 * 1024, "coefficient rows too long");
     const unsigned grid = (unsigned)(B < 148 * 32 ? B : 148 * 32);
     cudaStream_t st = (cudaStream_t)stream;
