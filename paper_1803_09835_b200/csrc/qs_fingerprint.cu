@@ -84,6 +84,12 @@ struct WinGeom {
     uint32_t frame, hop, nb, F, T, wmin, wmax, n_levels, top_k, mode;
 };
 
+// quotient by a warp-uniform divisor: a shift when it is a power of two (the
+// Haar block sizes and time bins usually are), else a division
+__device__ __forceinline__ uint32_t udiv_u(uint32_t p, uint32_t d) {
+    return (d & (d - 1)) == 0 ? p >> (__ffs(d) - 1) : p / d;
+}
+
 __device__ __forceinline__ uint64_t mag_key(double s) {
     return (uint64_t)__double_as_longlong(fabs(s));  // non-negative doubles order as integers
 }
@@ -276,18 +282,20 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
         for (uint32_t i = threadIdx.x; i < width * nb; i += blockDim.x) gs[i] = band[c0 * nb + i];
         __syncthreads();
         // frequency resample: tmp[Fi][w] = sum_f w_f[Fi, f] * band[w][f]
-        for (uint32_t i = threadIdx.x; i < F * width; i += blockDim.x) {
-            const uint32_t Fi = i / width, w = i - Fi * width;
-            double acc = 0.0;
-            for (int32_t e = wf_off[Fi]; e < wf_off[Fi + 1]; ++e)
-                acc = fma(wf_val[e], (double)gs[w * nb + wf_idx[e]], acc);
-            tmp[Fi * width + w] = acc;
+        for (uint32_t Fi = threadIdx.x >> 5; Fi < F; Fi += blockDim.x >> 5) {
+            const int32_t e0 = wf_off[Fi], e1 = wf_off[Fi + 1];
+            for (uint32_t w = threadIdx.x & 31; w < width; w += 32) {
+                double acc = 0.0;
+                for (int32_t e = e0; e < e1; ++e)
+                    acc = fma(wf_val[e], (double)gs[w * nb + wf_idx[e]], acc);
+                tmp[Fi * width + w] = acc;
+            }
         }
         __syncthreads();
         // time resample: img[Fi][Ti] = sum_w w_t[Ti, w] * tmp[Fi][w], stored f32
         const int32_t* to = wt_off + (uint64_t)(width - g.wmin) * (T + 1);
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint32_t Fi = i / T, Ti = i - Fi * T;
+            const uint32_t Fi = udiv_u(i, T), Ti = i - Fi * T;
             double acc = 0.0;
             for (int32_t e = to[Ti]; e < to[Ti + 1]; ++e) acc = fma(wt_val[e], tmp[Fi * width + wt_idx[e]], acc);
             img[i] = (double)(float)acc;
@@ -306,14 +314,14 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
             if (lmode & 1u) {  // rows (time axis)
                 const uint32_t half = w / 2;
                 for (uint32_t p = threadIdx.x; p < h * half; p += blockDim.x) {
-                    const uint32_t r = p / half, j = p - r * half;
+                    const uint32_t r = udiv_u(p, half), j = p - r * half;
                     const double ev = img[r * T + 2 * j], od = img[r * T + 2 * j + 1];
                     hs[r * T + j] = (ev + od) * s2;
                     hs[r * T + half + j] = (ev - od) * s2;
                 }
                 __syncthreads();
                 for (uint32_t p = threadIdx.x; p < h * w; p += blockDim.x) {
-                    const uint32_t r = p / w, c = p - r * w;
+                    const uint32_t r = udiv_u(p, w), c = p - r * w;
                     img[r * T + c] = hs[r * T + c];
                 }
                 __syncthreads();
@@ -321,14 +329,14 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
             if (lmode & 2u) {  // columns (frequency axis)
                 const uint32_t half = h / 2;
                 for (uint32_t p = threadIdx.x; p < half * w; p += blockDim.x) {
-                    const uint32_t i2 = p / w, c = p - i2 * w;
+                    const uint32_t i2 = udiv_u(p, w), c = p - i2 * w;
                     const double ev = img[(2 * i2) * T + c], od = img[(2 * i2 + 1) * T + c];
                     hs[i2 * T + c] = (ev + od) * s2;
                     hs[(half + i2) * T + c] = (ev - od) * s2;
                 }
                 __syncthreads();
                 for (uint32_t p = threadIdx.x; p < h * w; p += blockDim.x) {
-                    const uint32_t r = p / w, c = p - r * w;
+                    const uint32_t r = udiv_u(p, w), c = p - r * w;
                     img[r * T + c] = hs[r * T + c];
                 }
                 __syncthreads();
@@ -478,7 +486,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_haar_batch(double* __restrict__
                 if (rows) {
                     const uint32_t half = w / 2;
                     for (uint32_t p = threadIdx.x; p < h * half; p += blockDim.x) {
-                        const uint32_t r = p / half, j = p - r * half;
+                        const uint32_t r = udiv_u(p, half), j = p - r * half;
                         if (!inverse) {
                             const double ev = img[r * W + 2 * j], od = img[r * W + 2 * j + 1];
                             hs[r * W + j] = (ev + od) * s2;
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_haar_batch(double* __restrict__
                 } else {
                     const uint32_t half = h / 2;
                     for (uint32_t p = threadIdx.x; p < half * w; p += blockDim.x) {
-                        const uint32_t i2 = p / w, c = p - i2 * w;
+                        const uint32_t i2 = udiv_u(p, w), c = p - i2 * w;
                         if (!inverse) {
                             const double ev = img[(2 * i2) * W + c], od = img[(2 * i2 + 1) * W + c];
                             hs[i2 * W + c] = (ev + od) * s2;
@@ -506,7 +514,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_haar_batch(double* __restrict__
                 }
                 __syncthreads();
                 for (uint32_t p = threadIdx.x; p < h * w; p += blockDim.x) {
-                    const uint32_t r = p / w, c = p - r * w;
+                    const uint32_t r = udiv_u(p, w), c = p - r * w;
                     img[r * W + c] = hs[r * W + c];
                 }
                 __syncthreads();
