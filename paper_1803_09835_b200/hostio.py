@@ -21,7 +21,7 @@ def write_device_bytes(f, dev, chunk: int = CHUNK) -> None:
     if n == 0:
         return
     per = min(chunk, n)
-    bufs = [torch.empty(per, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    bufs = [torch.empty(per, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     evs = [torch.cuda.Event(), torch.cuda.Event()]
     spans = [(a, min(n, a + per)) for a in range(0, n, per)]
     for k, (a, b) in enumerate(spans[:2]):
@@ -44,7 +44,7 @@ def read_to_device(f, nbytes: int, chunk: int = CHUNK):
     if nbytes == 0:
         return out
     per = min(chunk, nbytes)
-    bufs = [torch.empty(per, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    bufs = [torch.empty(per, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     evs = [None, None]
     for k, a in enumerate(range(0, nbytes, per)):
         b = min(nbytes, a + per)

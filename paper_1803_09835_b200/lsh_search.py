@@ -507,7 +507,7 @@ def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
         return out
     dst = out.view(-1)
     per = max(1, chunk_bytes // flat.itemsize)
-    stage = [torch.empty(min(per, flat.size), dtype=dst.dtype).pin_memory() for _ in range(2)]
+    stage = [torch.empty(min(per, flat.size), dtype=dst.dtype, pin_memory=True) for _ in range(2)]
     done = [None, None]
     pool = _copy_pool()
     nthr = pool._max_workers
@@ -567,7 +567,7 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
     if n == 0:
         return keys, rkeys, tags, bad
     rows_per = max(1, chunk_bytes // (K * 4))
-    stage = [torch.empty((min(rows_per, n), K), dtype=torch.int32).pin_memory() for _ in range(2)]
+    stage = [torch.empty((min(rows_per, n), K), dtype=torch.int32, pin_memory=True) for _ in range(2)]
     done = [None, None]
     pool = _copy_pool()
     nthr = pool._max_workers
