@@ -185,16 +185,26 @@ int qs_lsh_compact_buckets(const uint32_t* sids_dev, const uint64_t* bstart_dev,
  * emit sim >= m; 1: emit only; 2: count only.  Emitted records are
  * (sortkey = (q - c) << 32 | c, sim) into out_key/out_sim (capacity cap; the
  * true count is always added to counters_dev[1] so the caller can grow and
- * retry); counters_dev[0] += distinct pairs. */
+ * retry); counters_dev[0] += distinct pairs.
+ * out_rest_dev (mode 1 only, may be NULL): lazy counts — a pair's count stops
+ * being confirmed once it reaches m; the candidate tables left unexamined are
+ * written as ceil(t/32) uint32 bit words per emitted pair and out_sim holds a
+ * partial count (>= m) until qs_lsh_complete_sims finishes it. */
 size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle);
 int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                  const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t n_nonsingle,
                  const uint64_t* rkeys_dev, const uint32_t* tags_dev, uint64_t n, uint32_t t,
                  uint32_t m, uint64_t excl, const uint8_t* excluded_dev,
                  const uint64_t* edges_dev, uint32_t p, int mode,
-                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint64_t cap,
-                 unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
+                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
+                 uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
                  void* stream);
+
+/* Exact counts of lazily counted pairs (see qs_lsh_pairs): pair_sim_dev[i] +=
+ * the agreeing tables among rest_dev[i * ceil(t/32) ...]. */
+int qs_lsh_complete_sims(const uint64_t* pair_key_dev, uint32_t* pair_sim_dev,
+                         const uint32_t* rest_dev, uint64_t n_pairs, const uint64_t* rkeys_dev,
+                         uint32_t t, void* stream);
 
 /* Occurrence filter (lsh_search.py:256-274) from the matched pairs of a
  * filter-free enumeration: per partition, degree over within-partition
@@ -221,11 +231,14 @@ int qs_lsh_occ_finish(uint8_t* excluded_dev, uint64_t n, unsigned long long* cou
                       void* stream);
 
 /* Matched pairs that survive the exclusion rule (pass-2 emission of
- * lsh_search.py:276-287), appended to out_* with *counter_dev as cursor. */
+ * lsh_search.py:276-287), appended to out_* with *counter_dev as cursor.
+ * rest_dev (may be NULL): the lazy-count words of each pair (rest_words per
+ * pair), carried along into out_rest_dev. */
 int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
-                        uint64_t n_pairs, const uint8_t* excluded_dev,
-                        const uint64_t* edges_dev, uint32_t p, uint64_t* out_key_dev,
-                        uint32_t* out_sim_dev, unsigned long long* counter_dev, void* stream);
+                        const uint32_t* rest_dev, uint32_t rest_words, uint64_t n_pairs,
+                        const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p,
+                        uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
+                        unsigned long long* counter_dev, void* stream);
 
 /* Sort matched pairs by (dt, idx1) (lsh_search.py:291) and pack them into
  * TRIPLET_DTYPE records (<u8 dt, <u8 idx1, <u4 sim; 20 bytes, :38).

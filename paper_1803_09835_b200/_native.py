@@ -55,12 +55,13 @@ SIGNATURES = {
                                        _p, _u32, _p, _u64, _p, _p, _sz, _p]),
     "qs_lsh_pairs_ws_bytes": (_sz, [_u64]),
     "qs_lsh_pairs": (_int, [_p, _p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
-                            _int, _p, _p, _u64, _p, _p, _sz, _p]),
+                            _int, _p, _p, _p, _u64, _p, _p, _sz, _p]),
+    "qs_lsh_complete_sims": (_int, [_p, _p, _p, _u64, _p, _u32, _p]),
     "qs_lsh_occurrence_filter": (_int, [_p, _p, _u64, _u64, _dbl, _p, _u32, _p, _p, _p, _p]),
     "qs_lsh_occ_degree": (_int, [_p, _u64, _p, _u32, _p, _p]),
     "qs_lsh_occ_mark": (_int, [_p, _u64, _p, _u64, _dbl, _p, _u32, _p, _p]),
     "qs_lsh_occ_finish": (_int, [_p, _u64, _p, _p]),
-    "qs_lsh_filter_pairs": (_int, [_p, _p, _u64, _p, _p, _u32, _p, _p, _p, _p]),
+    "qs_lsh_filter_pairs": (_int, [_p, _p, _p, _u32, _u64, _p, _p, _u32, _p, _p, _p, _p, _p]),
     "qs_sort_pairs_ws_bytes": (_sz, [_u64]),
     "qs_lsh_finalize": (_int, [_p, _p, _u64, _u32, _p, _p, _sz, _p]),
     "qs_fp_band_stft": (_int, [_p, _int, _u64, _u32, _u32, _u64, _u32, _p, _p, _p]),

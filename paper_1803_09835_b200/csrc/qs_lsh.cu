@@ -770,9 +770,11 @@ __global__ void k_occ_finish(uint8_t* __restrict__ ex, uint64_t n,
 
 // matched pairs of the filter-free pass that survive the exclusion rule
 __global__ void k_filter_pairs(const uint64_t* __restrict__ pk, const uint32_t* __restrict__ ps,
+                               const uint32_t* __restrict__ rest, uint32_t W,
                                uint64_t np, const uint8_t* __restrict__ ex,
                                const uint64_t* __restrict__ edges, uint32_t p,
                                uint64_t* __restrict__ opk, uint32_t* __restrict__ ops,
+                               uint32_t* __restrict__ orest,
                                unsigned long long* __restrict__ counter) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -783,6 +785,8 @@ __global__ void k_filter_pairs(const uint64_t* __restrict__ pk, const uint32_t* 
         const unsigned long long o = atomicAdd(counter, 1ULL);
         opk[o] = k;
         ops[o] = ps[i];
+        if (rest)
+            for (uint32_t w = 0; w < W; ++w) orest[o * W + w] = rest[i * W + w];
     }
 }
 
@@ -1010,14 +1014,16 @@ int qs_lsh_occurrence_filter(const uint64_t* pair_key_dev, const uint32_t* pair_
     return qs_lsh_occ_finish(excluded_dev, n, counters_dev, stream);
 }
 
-int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev, uint64_t n_pairs,
+int qs_lsh_filter_pairs(const uint64_t* pair_key_dev, const uint32_t* pair_sim_dev,
+                        const uint32_t* rest_dev, uint32_t rest_words, uint64_t n_pairs,
                         const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p,
-                        uint64_t* out_key_dev, uint32_t* out_sim_dev,
+                        uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
                         unsigned long long* counter_dev, void* stream) {
     if (n_pairs == 0) return QS_OK;
+    QS_ARG(!rest_dev || out_rest_dev, "out_rest_dev required with rest_dev");
     k_filter_pairs<<<qs_blocks(n_pairs, 256), 256, 0, (cudaStream_t)stream>>>(
-        pair_key_dev, pair_sim_dev, n_pairs, excluded_dev, edges_dev, p, out_key_dev, out_sim_dev,
-        counter_dev);
+        pair_key_dev, pair_sim_dev, rest_dev, rest_words, n_pairs, excluded_dev, edges_dev, p,
+        out_key_dev, out_sim_dev, out_rest_dev, counter_dev);
     QS_CHECK_LAUNCH("k_filter_pairs");
     return QS_OK;
 }

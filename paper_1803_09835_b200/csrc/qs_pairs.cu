@@ -230,6 +230,35 @@ __device__ __forceinline__ uint32_t confirm(const uint64_t* __restrict__ rkeys, 
     return hits;
 }
 
+// confirm() that stops once `need` tables agree: the tables it did not
+// examine stay in `cand` (lazy counts, completed later for surviving pairs)
+__device__ __forceinline__ uint32_t confirm_upto(const uint64_t* __restrict__ rkeys, uint32_t t,
+                                                 uint32_t a, uint32_t b, uint32_t& cand,
+                                                 uint32_t wbase, uint32_t need) {
+    uint32_t hits = 0;
+    const uint64_t* ra = rkeys + (uint64_t)a * t + wbase;
+    const uint64_t* rb = rkeys + (uint64_t)b * t + wbase;
+    while (cand && hits < need) {
+        uint32_t tt[4];
+        bool v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = cand != 0;
+            tt[k] = v[k] ? (uint32_t)(__ffs(cand) - 1) : 0u;
+            cand &= cand - 1;
+        }
+        uint64_t ka[4], kb[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            ka[k] = v[k] ? __ldg(ra + tt[k]) : 0;
+            kb[k] = v[k] ? __ldg(rb + tt[k]) : 1;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) hits += (ka[k] == kb[k]);
+    }
+    return hits;
+}
+
 // Queue entry flags (bits 0..7 = table & 0xFF, bits 16.. = table >> 8)
 constexpr uint32_t QF_COUNT = 1u << 8;     // needs the confirmed count (emit if >= m)
 constexpr uint32_t QF_DISTINCT = 1u << 9;  // count as a distinct pair when first
@@ -247,6 +276,7 @@ template <int W>
 __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cnt, uint32_t lane,
                                       const uint64_t* __restrict__ rkeys, uint32_t t, uint32_t m,
                                       uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim,
+                                      uint32_t* __restrict__ out_rest,
                                       uint64_t cap, unsigned long long* __restrict__ counters,
                                       unsigned long long& distinct) {
     if (lane < cnt) {
@@ -266,19 +296,34 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
         if (first) {
             if (f & QF_DISTINCT) ++distinct;
             if (f & QF_COUNT) {
+                // lazy (out_rest given, MATCHED): stop confirming once the pair
+                // reaches m and keep the unexamined candidate tables, so the
+                // exact count is completed only for pairs the filter keeps
+                const bool lazy = out_rest != nullptr;
                 uint32_t exact = 1;
+                uint32_t rest[W];
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
+                    rest[w] = 0;
                     if (w < wt) continue;
                     const uint32_t mw = q.qm[e * W + w];
-                    const uint32_t x = (w == wt) ? (mw & ~((low << 1) | 1u)) : mw;
-                    if (x) exact += confirm(rkeys, t, a, b, x, w * 32, false);
+                    uint32_t x = (w == wt) ? (mw & ~((low << 1) | 1u)) : mw;
+                    if (lazy) {
+                        if (x && exact < m) exact += confirm_upto(rkeys, t, a, b, x, w * 32, m - exact);
+                        rest[w] = x;
+                    } else if (x) {
+                        exact += confirm(rkeys, t, a, b, x, w * 32, false);
+                    }
                 }
                 if (exact >= m) {
                     const unsigned long long pos = atomicAdd(counters + 1, 1ULL);
                     if (pos < cap) {
                         out_key[pos] = ((uint64_t)(b - a) << 32) | a;
                         out_sim[pos] = exact;
+                        if (lazy) {
+#pragma unroll
+                            for (int w = 0; w < W; ++w) out_rest[pos * W + w] = rest[w];
+                        }
                     }
                 }
             }
@@ -344,9 +389,9 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
     const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab, Plan plan,
     const uint64_t* __restrict__ rkeys, const uint32_t* __restrict__ tags, uint64_t n, uint32_t t,
     uint32_t m, uint64_t excl, const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges,
-    uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
-    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ work, uint32_t tmax,
-    uint32_t wg) {
+    uint32_t p, uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim,
+    uint32_t* __restrict__ out_rest, uint64_t cap, unsigned long long* __restrict__ counters,
+    unsigned long long* __restrict__ work, uint32_t tmax, uint32_t wg) {
     // W = tag words staged per row (words 0..W-1); wg = words per row in `tags`;
     // WT = the launch's table word (DISTINCT / FULL are launched per word)
     using C = TileCfg<W, MODE, WT>;
@@ -686,8 +731,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         __syncwarp();
                         PROF_STOP(1)
                         PROF_START
-                        drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, cap, counters,
-                                 distinct);
+                        drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
+                                 counters, distinct);
                         PROF_STOP(2)
                         PROF_START
                         qhead = (qhead + 32) & (QCAP - 1);
@@ -723,7 +768,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
         if (lane == 0) mbar_arrive(&empty_bar[bsel]);
     }
     __syncwarp();
-    if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, cap, counters, distinct);
+    if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
+                     distinct);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
     if (lane == 0 && distinct) atomicAdd(counters + 0, distinct);
@@ -829,8 +875,8 @@ __global__ void __launch_bounds__(256) k_pairs_generic(
     const uint64_t* __restrict__ chunk_off, uint64_t nb, const uint64_t* __restrict__ rkeys,
     const uint32_t* __restrict__ tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
     const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges, uint32_t p, int mode,
-    uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint64_t cap,
-    unsigned long long* __restrict__ counters) {
+    uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim,
+    uint32_t* __restrict__ out_rest, uint64_t cap, unsigned long long* __restrict__ counters) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gwarp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -876,7 +922,9 @@ __global__ void __launch_bounds__(256) k_pairs_generic(
                 const unsigned long long pos = atomicAdd(counters + 1, 1ULL);
                 if (pos < cap) {
                     out_key[pos] = (dt << 32) | a;
-                    out_sim[pos] = exact;
+                    out_sim[pos] = exact;  // exact: nothing left to complete
+                    if (out_rest)
+                        for (uint32_t w = 0; w < W; ++w) out_rest[pos * W + w] = 0;
                 }
             }
         }
@@ -899,8 +947,8 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
                   const uint32_t* btab, uint64_t nb, const uint64_t* rkeys, const uint32_t* tags,
                   uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
                   const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
-                  uint64_t cap, unsigned long long* counters, uint64_t* ws, void* sws,
-                  cudaStream_t st, uint32_t wg) {
+                  uint32_t* out_rest, uint64_t cap, unsigned long long* counters, uint64_t* ws,
+                  void* sws, cudaStream_t st, uint32_t wg) {
     using C = TileCfg<W, MODE, WT>;
     const uint32_t L = C::L;
     uint64_t* mpre = ws;                       // nb + 1
@@ -938,7 +986,8 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     if (per_sm < 1) per_sm = 1;
     kern<<<num_sms() * per_sm, PTHREADS, C::SMEM, st>>>(sids, bstart, bsize, btab, plan, rkeys, tags,
                                                         n, t, m, excl, emask, edges, p, out_key,
-                                                        out_sim, cap, counters, work, tmax, wg);
+                                                        out_sim, out_rest, cap, counters, work,
+                                                        tmax, wg);
     QS_CHECK_LAUNCH("k_pairs_pc");
     return QS_OK;
 }
@@ -966,8 +1015,8 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
                           const uint32_t* btab, uint64_t nb, const uint64_t* rkeys,
                           const uint32_t* tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
                           const uint8_t* emask, const uint64_t* edges, uint32_t p, uint64_t* ok,
-                          uint32_t* os, uint64_t cap, unsigned long long* counters, uint64_t* ws,
-                          void* sws, cudaStream_t st) {
+                          uint32_t* os, uint32_t* orest, uint64_t cap,
+                          unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
     uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
     k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
     uint64_t hb[5] = {0, 0, 0, 0, 0};
@@ -979,7 +1028,8 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
         if (MODE == MODE_MATCHED && 32 * w > t - m) continue;  // no first collision there
 #define QS_W(WW, WTT)                                                                             \
     run_pc<WW, MODE, HAS_E, WTT>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
-                                 m, excl, emask, edges, p, ok, os, cap, counters, ws, sws, st, W)
+                                 m, excl, emask, edges, p, ok, os, orest, cap, counters, ws, sws, \
+                                 st, W)
         constexpr bool DI = MODE == MODE_DISTINCT;
         int rc = QS_OK;
         if (w == 0) {
@@ -1002,19 +1052,38 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
                          const uint32_t* bsize, const uint32_t* btab, uint64_t nb,
                          const uint64_t* rkeys, const uint32_t* tags, uint64_t n, uint32_t t,
                          uint32_t m, uint64_t excl, const uint8_t* emask, const uint64_t* edges,
-                         uint32_t p, uint64_t* ok, uint32_t* os, uint64_t cap,
+                         uint32_t p, uint64_t* ok, uint32_t* os, uint32_t* orest, uint64_t cap,
                          unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
 #define QS_L(MM, EE) \
     run_pc<W, MM, EE, 0>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, \
-                         p, ok, os, cap, counters, ws, sws, st, W)
+                         p, ok, os, orest, cap, counters, ws, sws, st, W)
 #define QS_D(MM, EE) \
     run_word_split<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
-                              edges, p, ok, os, cap, counters, ws, sws, st)
+                              edges, p, ok, os, orest, cap, counters, ws, sws, st)
+    if (mode != MODE_MATCHED) orest = nullptr;  // lazy counts: MATCHED only
     if (mode == MODE_FULL) return has_e ? QS_D(MODE_FULL, true) : QS_D(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_D(MODE_MATCHED, true) : QS_D(MODE_MATCHED, false);
     return has_e ? QS_D(MODE_DISTINCT, true) : QS_D(MODE_DISTINCT, false);
 #undef QS_L
 #undef QS_D
+}
+
+// exact counts of lazily counted pairs: the candidate tables the drain left
+// unexamined (rest, W words per pair) are confirmed on the keys now
+__global__ void k_complete_sims(const uint64_t* __restrict__ pk, uint32_t* __restrict__ ps,
+                                const uint32_t* __restrict__ rest, uint64_t np,
+                                const uint64_t* __restrict__ rkeys, uint32_t t, uint32_t W) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t add = 0;
+        const uint64_t k = pk[i];
+        const uint32_t a = (uint32_t)k, b = a + (uint32_t)(k >> 32);
+        for (uint32_t w = 0; w < W; ++w) {
+            const uint32_t x = rest[i * W + w];
+            if (x) add += confirm(rkeys, t, a, b, x, w * 32, false);
+        }
+        if (add) ps[i] += add;
+    }
 }
 
 }  // namespace qs
@@ -1046,7 +1115,7 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
                  const uint32_t* btab_dev, uint64_t n_nonsingle, const uint64_t* rkeys_dev,
                  const uint32_t* tags_dev, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
                  const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
-                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint64_t cap,
+                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev, uint64_t cap,
                  unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     QS_ARG(ws_bytes >= qs_lsh_pairs_ws_bytes(n_nonsingle), "pairs workspace too small");
@@ -1061,7 +1130,7 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
 #define QS_D(WW)                                                                                  \
     dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, nb, rkeys_dev,      \
                       tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,           \
-                      out_sim_dev, cap, counters_dev, ws, sws, st)
+                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, st)
     switch (W) {
         case 1: return QS_D(1);
         case 2: return QS_D(2);
@@ -1074,12 +1143,24 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
             if (rc) return rc;
             k_pairs_generic<<<num_sms() * 8, 256, 0, st>>>(
                 sids_dev, bstart_dev, bsize_dev, btab_dev, off, nb, rkeys_dev, tags_dev, n, t, m,
-                excl, excluded_dev, edges_dev, p, mode, out_key_dev, out_sim_dev, cap, counters_dev);
+                excl, excluded_dev, edges_dev, p, mode, out_key_dev, out_sim_dev,
+                mode == MODE_MATCHED ? out_rest_dev : nullptr, cap, counters_dev);
             QS_CHECK_LAUNCH("k_pairs_generic");
             return QS_OK;
         }
     }
 #undef QS_D
+}
+
+int qs_lsh_complete_sims(const uint64_t* pair_key_dev, uint32_t* pair_sim_dev,
+                         const uint32_t* rest_dev, uint64_t n_pairs, const uint64_t* rkeys_dev,
+                         uint32_t t, void* stream) {
+    if (n_pairs == 0) return QS_OK;
+    QS_ARG(t >= 1, "t must be >= 1");
+    k_complete_sims<<<qs_blocks(n_pairs, 256), 256, 0, (cudaStream_t)stream>>>(
+        pair_key_dev, pair_sim_dev, rest_dev, n_pairs, rkeys_dev, t, (t + 31) >> 5);
+    QS_CHECK_LAUNCH("k_complete_sims");
+    return QS_OK;
 }
 
 }  // extern "C"

@@ -29,6 +29,8 @@ TRIPLET_DTYPE = np.dtype([("dt", "<u8"), ("idx1", "<u8"), ("sim", "<u4")])
 PROFILES = {"baseline": (6, 5), "optimized": (8, 2)}
 
 _HIST_LEN = 1 << 16
+# MATCHED pass counts lazily (exact sims completed for filter survivors only)
+_LAZY_COUNTS = os.environ.get("QS_LAZY_COUNTS", "1") != "0"
 _cap_hint = {}
 
 
@@ -249,14 +251,18 @@ class DeviceSearch:
             cap = max(1 << 16, _cap_hint.get(key, 4 * self.n))
         counters = torch.zeros(2, dtype=torch.int64, device=self.dev)
         ws = self._empty(lib.qs_lsh_pairs_ws_bytes(nb))
+        lazy = mode == self.MODE_MATCHED and _LAZY_COUNTS
+        W = (self.t + 31) // 32
         while True:
             pk = torch.empty(max(cap, 1), dtype=torch.int64, device=self.dev)
             ps = torch.empty(max(cap, 1), dtype=torch.int32, device=self.dev)
+            rest = torch.empty(max(cap, 1) * W, dtype=torch.int32, device=self.dev) if lazy else None
             counters.zero_()
             nat.call("qs_lsh_pairs", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize), nat.ptr(btab),
                      nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n, self.t, m, excl,
-                     nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk), nat.ptr(ps), cap,
-                     nat.ptr(counters), nat.ptr(ws), ws.numel(), nat.stream())
+                     nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk), nat.ptr(ps),
+                     nat.ptr(rest), cap, nat.ptr(counters), nat.ptr(ws), ws.numel(),
+                     nat.stream())
             # word bounds + per launched table word: 7 planning kernels, 2x3 scan kernels, pairs
             words = (self.t + 31) // 32
             if mode == self.MODE_MATCHED:
@@ -268,7 +274,23 @@ class DeviceSearch:
             cap = int(matched * 1.1) + 1024
         if mode != self.MODE_DISTINCT:
             _cap_hint[key] = max(_cap_hint.get(key, 0), int(matched * 1.1) + 1024)
-        return pk[:matched], ps[:matched], matched, distinct
+        pk, ps = pk[:matched], ps[:matched]
+        # lazily counted sims travel with this pk until complete_sims()
+        self._lazy = (pk, rest[: matched * W]) if lazy else None
+        return pk, ps, matched, distinct
+
+    def complete_sims(self, pk, ps, matched):
+        """Exact sims for lazily counted MATCHED pairs (the tables left
+        unexamined once a pair reached m are confirmed now, for the pairs that
+        survived the filter only)."""
+        lz = getattr(self, "_lazy", None)
+        if lz is None or lz[0] is not pk:
+            return
+        if matched:
+            nat.call("qs_lsh_complete_sims", nat.ptr(pk), nat.ptr(ps), nat.ptr(lz[1]), matched,
+                     nat.ptr(self.rkeys), self.t, nat.stream())
+            self.launches += 1
+        self._lazy = None
 
     def occurrence(self, pk, ps, matched, threshold, edges, p):
         torch = self.torch
@@ -310,11 +332,19 @@ class DeviceSearch:
         opk = torch.empty(max(matched, 1), dtype=torch.int64, device=self.dev)
         ops = torch.empty(max(matched, 1), dtype=torch.int32, device=self.dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        nat.call("qs_lsh_filter_pairs", nat.ptr(pk), nat.ptr(ps), matched, nat.ptr(emask),
-                 nat.ptr(edges), p, nat.ptr(opk), nat.ptr(ops), nat.ptr(cnt), nat.stream())
+        lz = getattr(self, "_lazy", None)
+        rest = lz[1] if lz is not None and lz[0] is pk else None
+        W = (self.t + 31) // 32
+        orest = torch.empty(max(matched, 1) * W, dtype=torch.int32, device=self.dev) if rest is not None else None
+        nat.call("qs_lsh_filter_pairs", nat.ptr(pk), nat.ptr(ps), nat.ptr(rest), W, matched,
+                 nat.ptr(emask), nat.ptr(edges), p, nat.ptr(opk), nat.ptr(ops), nat.ptr(orest),
+                 nat.ptr(cnt), nat.stream())
         self.launches += 1
         k = int(cnt.item())
-        return opk[:k], ops[:k], k
+        opk, ops = opk[:k], ops[:k]
+        if rest is not None:
+            self._lazy = (opk, orest[: k * W])
+        return opk, ops, k
 
     def bucket_stats(self, emask, edges, p):
         torch = self.torch
@@ -409,6 +439,7 @@ def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_w
                 del lists
             else:
                 _, _, _, distinct = ds.pairs(ds.MODE_DISTINCT, m, excl, emask, edges, p)
+    ds.complete_sims(pk, ps, matched)
     looks, pieces, mx, hist, big = ds.bucket_stats(emask, edges, p)
     trip = ds.finalize(pk, ps, matched)
     fill_stats(stats, n, t, looks, pieces, mx, hist, big, ds.heads - ds.nb, distinct, matched, n_ex)

@@ -136,6 +136,7 @@ def run_search_sharded(engine, comm, n: int, t: int, cfg, exclusion_windows: int
                 del lists
             else:
                 _, _, _, distinct = engine.pairs(engine.MODE_DISTINCT, m, excl, emask, edges, p)
+    engine.complete_sims(pk, ps, matched)
     looks, pieces, mx, hist, big = engine.bucket_stats(emask, edges, p)
     singles = engine.heads - engine.nb
     tot = torch.tensor([distinct, looks, pieces, singles, matched], dtype=torch.int64,

@@ -153,6 +153,10 @@ class NumpyShardEngine:
             looks += lb - (s - e_tot)
         return looks, pieces, mx, hist, np.array(big, dtype=np.int64)
 
+    def complete_sims(self, pk, ps, matched):
+        """Sims here are exact already (DeviceSearch counts MATCHED lazily)."""
+        return None
+
     def finalize(self, pk, ps, matched):
         k = pk[:matched].numpy().astype(np.uint64)
         s = ps[:matched].numpy().astype(np.uint32)
