@@ -276,7 +276,8 @@ class DeviceSearch:
             _cap_hint[key] = max(_cap_hint.get(key, 0), int(matched * 1.1) + 1024)
         pk, ps = pk[:matched], ps[:matched]
         # lazily counted sims travel with this pk until complete_sims()
-        self._lazy = (pk, rest[: matched * W]) if lazy else None
+        if lazy:
+            self._lazy = (pk, rest[: matched * W])
         return pk, ps, matched, distinct
 
     def complete_sims(self, pk, ps, matched):
