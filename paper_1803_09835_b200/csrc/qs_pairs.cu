@@ -341,20 +341,31 @@ __device__ __forceinline__ uint2 make_chunk(uint32_t abase, uint32_t acnt, uint3
 __device__ __forceinline__ uint32_t n_pieces(uint32_t bb, uint32_t be) {
     return be > bb ? (be - bb + BPIECE - 1) / BPIECE : 0;
 }
-// all chunks of the rows [off, off + s) of one bucket (pairs j > i)
-__device__ __forceinline__ uint32_t count_chunks_tri(uint32_t s) {
+// all chunks of the rows [off, off + s) of one bucket (pairs j > i): per
+// 32-row A group one FOLD chunk for the pairs inside the group (lane i meets
+// row i + d mod acnt, d = 1 .. acnt / 2: the triangle in acnt / 2 steps with
+// every lane busy) and rectangular pieces for the later rows
+// (fold = false: triangle pieces from row i + 1 with per-lane validity, the
+// MATCHED pass's choice — measured faster there, its broadcast row loads
+// matter more than the idle lanes)
+__device__ __forceinline__ uint32_t count_chunks_tri(uint32_t s, bool fold) {
     uint32_t n = 0;
-    for (uint32_t c = 0; c * 32 < s; ++c) n += n_pieces(c * 32 + 1, s);
+    for (uint32_t c = 0; c * 32 < s; ++c) {
+        const uint32_t acnt = min(32u, s - c * 32);
+        n += fold ? (acnt >= 2 ? 1u : 0u) + n_pieces(c * 32 + acnt, s) : n_pieces(c * 32 + 1, s);
+    }
     return n;
 }
 __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, uint32_t off,
-                                                uint32_t s, uint32_t table) {
+                                                uint32_t s, uint32_t table, bool fold) {
     for (uint32_t c = 0; c * 32 < s; ++c) {
         const uint32_t ab = off + c * 32, acnt = min(32u, s - c * 32);
-        const uint32_t np = n_pieces(c * 32 + 1, s);
+        if (fold && acnt >= 2) chunks[base++] = make_chunk(ab, acnt, 0, 0, true, table);
+        const uint32_t first = fold ? acnt : 1;
+        const uint32_t np = n_pieces(c * 32 + first, s);
         for (uint32_t k = 0; k < np; ++k) {
-            const uint32_t b0 = ab + 1 + k * BPIECE;
-            chunks[base++] = make_chunk(ab, acnt, b0, min(off + s, b0 + BPIECE), true, table);
+            const uint32_t b0 = ab + first + k * BPIECE;
+            chunks[base++] = make_chunk(ab, acnt, b0, min(off + s, b0 + BPIECE), !fold, table);
         }
     }
 }
@@ -398,6 +409,14 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
     using Lay = typename C::Lay;
     constexpr int NP = C::NP;
     constexpr uint32_t L = C::L;
+#ifndef QS_FOLD_MATCHED
+#define QS_FOLD_MATCHED 0
+#endif
+#ifndef QS_FOLD_OFF
+    constexpr bool FOLD = MODE != MODE_MATCHED || QS_FOLD_MATCHED;  // fold chunks for triangles
+#else
+    constexpr bool FOLD = false;
+#endif
     extern __shared__ __align__(128) unsigned char psm[];
     __shared__ __align__(8) uint64_t full_bar[NBUF], empty_bar[NBUF];
     __shared__ uint32_t s_nch[C::NMETA], s_next[C::NMETA], s_nrows[C::NMETA];
@@ -472,8 +491,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         const uint32_t off = (uint32_t)(mp0 - mbase);
                         p_off[kk] = off;
                         p_st[kk] = __ldg(bstart + b0 + i);
-                        const uint32_t cb = atomicAdd(&s_nch[ma], count_chunks_tri(s));
-                        emit_chunks_tri(chunks, cb, off, s, __ldg(btab + b0 + i));
+                        const uint32_t cb = atomicAdd(&s_nch[ma], count_chunks_tri(s, FOLD));
+                        emit_chunks_tri(chunks, cb, off, s, __ldg(btab + b0 + i), FOLD);
                     }
                     nsb += __popc(bal);
                 }
@@ -529,8 +548,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     const uint32_t table = btab[bk];
                     uint32_t cbase = 0;
                     if (J == I) {
-                        emit_chunks_tri(chunks, 0, 0, nI, table);
-                        cbase = count_chunks_tri(nI);
+                        emit_chunks_tri(chunks, 0, 0, nI, table, FOLD);
+                        cbase = count_chunks_tri(nI, FOLD);
                     } else {
                         for (uint32_t c = 0; c * 32 < nI; ++c) {
                             const uint32_t np = n_pieces(nI, nI + nJ);
@@ -643,18 +662,36 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 a_ok = emask[a] == 0;
                 a_part = p > 1 ? part_of(edges, p, a) : 0;
             }
-            const uint32_t u_lo = tri ? apos + 1 : bbeg;  // pairs j > i within a bucket
             const bool excl_on = excl > 0;
-            // evaluate the pair (a, row u): validity, tag-plane masks, queue decision
-            auto eval = [&](uint32_t u, const uint32_t* R, bool& slow, uint32_t& flags,
-                            uint32_t (&qmask)[W]) {
-                bool valid = a_ok && u >= u_lo;
-                if (excl_on || HAS_E) {
-                    const uint32_t bid = ids[u];
-                    valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend within a bucket
-                    if (HAS_E && valid && emask[bid] &&
-                        (p <= 1 || part_of(edges, p, bid) == a_part))
-                        valid = false;
+            // evaluate the pair (a, row u): validity, tag-plane masks, queue decision.
+            // Rectangular chunks: row u lies after every A row (its id is larger).
+            // Fold chunks: row u may precede the lane's row, so the pair is taken
+            // in canonical (smaller id, larger id) order.
+            auto eval = [&](uint32_t u, const uint32_t* R, bool fold, bool fold_ok, bool& slow,
+                            uint32_t& flags, uint32_t (&qmask)[W]) {
+                bool valid;
+                if (fold) {
+                    valid = fold_ok;
+                    if (excl_on || HAS_E) {
+                        const uint32_t bid = ids[u];
+                        const uint32_t c = min(a, bid), qv = max(a, bid);
+                        valid = valid && (uint64_t)(qv - c) > excl;
+                        if (HAS_E && valid) {
+                            if (emask[c]) valid = false;
+                            else if (emask[qv] && (p <= 1 || part_of(edges, p, qv) ==
+                                                                 part_of(edges, p, c)))
+                                valid = false;
+                        }
+                    }
+                } else {
+                    valid = a_ok && u >= (tri ? apos + 1 : bbeg);  // tri: pairs j > i
+                    if (excl_on || HAS_E) {
+                        const uint32_t bid = ids[u];
+                        valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend within a bucket
+                        if (HAS_E && valid && emask[bid] &&
+                            (p <= 1 || part_of(edges, p, bid) == a_part))
+                            valid = false;
+                    }
                 }
                 slow = false;
                 flags = tflag;
@@ -709,7 +746,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 }
             };
             // queue the warp's slow lanes; drain 32 once the queue holds 32
-            auto push = [&](uint32_t u, const uint32_t* R, bool slow, uint32_t flags,
+            auto push = [&](uint32_t u, const uint32_t* R, bool fold, bool slow, uint32_t flags,
                             uint32_t (&qmask)[W]) {
                 const uint32_t bal = __ballot_sync(0xffffffffu, slow);
                 if (bal) {
@@ -720,8 +757,9 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     }
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
-                        q.qa[e] = a;
-                        q.qb[e] = ids[u];
+                        const uint32_t bid = ids[u];
+                        q.qa[e] = fold ? min(a, bid) : a;
+                        q.qb[e] = fold ? max(a, bid) : bid;
                         q.qt[e] = flags;
 #pragma unroll
                         for (int w = 0; w < W; ++w) q.qm[e * W + w] = qmask[w];
@@ -740,27 +778,31 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     }
                 }
             };
-            uint32_t u = bbeg;
-            const uint32_t* R = rows + bbeg * C::ROWP;
-#ifndef QS_UNROLL_M
-#define QS_UNROLL_M 0
-#endif
-            if (MODE == MODE_MATCHED && QS_UNROLL_M) {
-                // two B rows per step: independent LOP3 chains overlap their latencies
-                for (; u + 1 < bend; u += 2, R += 2 * C::ROWP) {
-                    bool s0, s1;
-                    uint32_t f0, f1, m0[W], m1[W];
-                    eval(u, R, s0, f0, m0);
-                    eval(u + 1, R + C::ROWP, s1, f1, m1);
-                    push(u, R, s0, f0, m0);
-                    push(u + 1, R + C::ROWP, s1, f1, m1);
+            if (FOLD && tri) {
+                // fold chunk: the pairs among the chunk's own acnt rows, lane i
+                // against row i + dd (mod acnt); at dd = acnt / 2 (even acnt) the
+                // lanes i < dd cover every pair once
+                const uint32_t nst = acnt >> 1;
+                for (uint32_t dd = 1; dd <= nst; ++dd) {
+                    uint32_t j = lane + dd;
+                    if (j >= acnt) j -= acnt;
+                    const bool ok = active && (2 * dd != acnt || lane < dd);
+                    const uint32_t u = abase + (active ? j : 0);
+                    const uint32_t* R = rows + u * C::ROWP;
+                    bool s0;
+                    uint32_t f0, m0[W];
+                    eval(u, R, true, ok, s0, f0, m0);
+                    push(u, R, true, s0, f0, m0);
                 }
-            }
-            for (; u < bend; ++u, R += C::ROWP) {
-                bool s0;
-                uint32_t f0, m0[W];
-                eval(u, R, s0, f0, m0);
-                push(u, R, s0, f0, m0);
+            } else {
+                uint32_t u = bbeg;
+                const uint32_t* R = rows + bbeg * C::ROWP;
+                for (; u < bend; ++u, R += C::ROWP) {
+                    bool s0;
+                    uint32_t f0, m0[W];
+                    eval(u, R, false, false, s0, f0, m0);
+                    push(u, R, false, s0, f0, m0);
+                }
             }
         }
         __syncwarp();
