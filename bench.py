@@ -456,7 +456,8 @@ def run_ours(args):
                            ("n_total" if tables_mode else "n_per_gpu"): n,
                            "d": 4096, "set_bits": 400, "tables": 100, "hash_funcs": 4,
                            "min_matches": 5, "occurrence_threshold": occ, "partitions": 1,
-                           "l2": "inputs (12.8 GB bits) larger than L2; no flush",
+                           "l2": f"inputs ({n * 400 * 4 / 1e9:.1f} GB bits) larger than L2 "
+                                 "(126 MB); no flush",
                            "parallelism": (f"table-sharded x{world} (round-robin tables, "
                                            "row-sharded Min-Max + NCCL all-gather)" if tables_mode
                                            else f"station-sharded x{world}")},
