@@ -35,13 +35,22 @@ constexpr uint32_t PLAN_MAX_D = 16384;  // smem bitonic sort capacity (192 KB)
 static inline size_t plan_order_bytes(uint32_t d, uint32_t F) {
     return (((size_t)2 * d * F * sizeof(uint16_t)) + 255) & ~(size_t)255;
 }
+// The first PLAN_BLK ranks of every probe sequence again, rank-block-major:
+// blk[b][seq] = ranks 8b .. 8b + 7 of sequence seq (16 bytes).  Lanes of a warp
+// mostly sit in the first blocks of neighbouring sequences, so these loads
+// coalesce where the sequence-major rows scatter over 32 lines.
+constexpr uint32_t PLAN_BLK = 32;
+static inline size_t plan_blk_offset(uint32_t d, uint32_t F) {
+    return plan_order_bytes(d, F) + (size_t)2 * d * F * sizeof(uint64_t);
+}
 
 // One CTA per hash column: bitonic sort of (value, element) in shared memory,
 // then write both probe directions of the column into the plan.
 __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, uint32_t d,
                                                uint32_t F, uint32_t dpad,
                                                uint16_t* __restrict__ order,
-                                               uint64_t* __restrict__ svals) {
+                                               uint64_t* __restrict__ svals,
+                                               uint16_t* __restrict__ blk) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* key = (uint64_t*)smem;
     uint32_t* idx = (uint32_t*)(key + dpad);
@@ -74,6 +83,11 @@ __global__ void __launch_bounds__(1024) k_plan(const uint64_t* __restrict__ v, u
             __syncthreads();
         }
     }
+    if (blk != nullptr)
+        for (uint32_t r = threadIdx.x; r < PLAN_BLK && r < d; r += blockDim.x) {
+            blk[((uint64_t)(r >> 3) * 2 * F + f) * 8 + (r & 7)] = (uint16_t)idx[r];
+            blk[((uint64_t)(r >> 3) * 2 * F + F + f) * 8 + (r & 7)] = (uint16_t)idx[d - 1 - r];
+        }
     for (uint32_t r = threadIdx.x; r < d; r += blockDim.x) {
         const uint64_t up = (uint64_t)f * d + r, down = ((uint64_t)F + f) * d + r;
         // the combine step only ever uses fmix64(value): store it pre-mixed
@@ -97,7 +111,8 @@ __global__ void __launch_bounds__(256) k_signatures(
     const uint16_t* __restrict__ order, const uint64_t* __restrict__ svals, uint32_t d,
     uint32_t F, uint32_t t, uint32_t kh, uint64_t* __restrict__ sigs,
     uint64_t* __restrict__ keys, uint64_t* __restrict__ rkeys, uint32_t* __restrict__ tags,
-    uint32_t* __restrict__ bad, uint64_t row0, uint64_t row_end) {
+    uint32_t* __restrict__ bad, uint64_t row0, uint64_t row_end,
+    const uint4* __restrict__ blk) {
     // rows [row0, row_end) of an n-row layout (n: the stride of keys / tags)
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t words = (d + 31) >> 5;
@@ -142,7 +157,9 @@ __global__ void __launch_bounds__(256) k_signatures(
         const uint16_t* ord = order + (uint64_t)seq * d;
         if ((d & 7) == 0) {
             while (seq < 2 * F) {
-                const uint4 v = __ldg((const uint4*)(ord + r));
+                const uint4 v = (blk != nullptr && r < PLAN_BLK)
+                                    ? __ldg(blk + (r >> 3) * 2 * F + seq)
+                                    : __ldg((const uint4*)(ord + r));
                 const uint32_t w[4] = {v.x, v.y, v.z, v.w};
                 uint32_t h = 0;
 #pragma unroll
@@ -229,6 +246,9 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     const uint32_t F = t * kh;
     const uint16_t* order = (const uint16_t*)plan;
     const uint64_t* svals = (const uint64_t*)((const unsigned char*)plan + plan_order_bytes(d, F));
+    const uint4* blk = d >= PLAN_BLK && (d & 7) == 0
+                           ? (const uint4*)((const unsigned char*)plan + plan_blk_offset(d, F))
+                           : nullptr;
     size_t per_warp = sig_smem_per_warp(d, F);
     int warps = 8;
     while (warps > 1 && per_warp * warps > 200 * 1024) warps >>= 1;
@@ -252,11 +272,11 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     if (search)
         k_signatures<true><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
                                                          sigs, keys, rkeys, tags, bad, row0,
-                                                         row0 + nrows);
+                                                         row0 + nrows, blk);
     else
         k_signatures<false><<<grid, threads, smem, st>>>(bits, n, K, order, svals, d, F, t, kh,
                                                           sigs, nullptr, nullptr, nullptr, bad,
-                                                          row0, row0 + nrows);
+                                                          row0, row0 + nrows, blk);
     QS_CHECK_LAUNCH("k_signatures");
     return QS_OK;
 }
@@ -277,7 +297,7 @@ int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs, uint
 }
 
 size_t qs_minmax_plan_bytes(uint32_t d, uint32_t n_funcs) {
-    return plan_order_bytes(d, n_funcs) + (size_t)2 * d * n_funcs * sizeof(uint64_t);
+    return plan_blk_offset(d, n_funcs) + (size_t)2 * n_funcs * PLAN_BLK * sizeof(uint16_t);
 }
 
 int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs, void* plan_dev,
@@ -293,7 +313,11 @@ int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs, voi
     uint16_t* order = (uint16_t*)plan_dev;
     uint64_t* svals = (uint64_t*)((unsigned char*)plan_dev + plan_order_bytes(d, n_funcs));
     unsigned threads = dpad >= 1024 ? 1024 : dpad;
-    k_plan<<<n_funcs, threads, smem, (cudaStream_t)stream>>>(values_dev, d, n_funcs, dpad, order, svals);
+    uint16_t* blk = d >= PLAN_BLK && (d & 7) == 0
+                        ? (uint16_t*)((unsigned char*)plan_dev + plan_blk_offset(d, n_funcs))
+                        : nullptr;
+    k_plan<<<n_funcs, threads, smem, (cudaStream_t)stream>>>(values_dev, d, n_funcs, dpad, order, svals,
+                                                             blk);
     QS_CHECK_LAUNCH("k_plan");
     return QS_OK;
 }

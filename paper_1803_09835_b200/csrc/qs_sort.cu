@@ -13,7 +13,10 @@ namespace qs {
 #define QS_RS_THREADS 256
 #endif
 constexpr int RS_THREADS = QS_RS_THREADS;
-constexpr int RS_ITEMS = 16;
+#ifndef QS_RS_ITEMS
+#define QS_RS_ITEMS 16
+#endif
+constexpr int RS_ITEMS = QS_RS_ITEMS;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per tile
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_RADIX = 256;
@@ -172,7 +175,10 @@ __global__ void __launch_bounds__(RSC_T) k_rs_scan_down(uint32_t* __restrict__ a
 // Stable scatter of one tile: rank in input order per digit, stage the tile in
 // shared memory in (digit, input) order, then write each digit's run to its
 // global slot with consecutive threads on consecutive addresses (coalesced).
-__global__ void __launch_bounds__(RS_THREADS, 2) k_rs_scatter(
+#ifndef QS_RS_MINB
+#define QS_RS_MINB 2
+#endif
+__global__ void __launch_bounds__(RS_THREADS, QS_RS_MINB) k_rs_scatter(
     const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t seg_len,
     uint32_t tiles, uint32_t shift, const uint32_t* __restrict__ offs,
     uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals) {
