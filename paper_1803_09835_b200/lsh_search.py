@@ -523,7 +523,8 @@ def _copy_pool():
     global _COPY_POOL
     if _COPY_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _COPY_POOL = ThreadPoolExecutor(max(1, min(8, len(os.sched_getaffinity(0)))))
+        want = int(os.environ.get("QS_COPY_THREADS", "8"))
+        _COPY_POOL = ThreadPoolExecutor(max(1, min(want, len(os.sched_getaffinity(0)))))
     return _COPY_POOL
 
 
