@@ -48,7 +48,7 @@ def _oracle(sigs, cfg, excl):
                       exclusion_windows=excl)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(24))
 def test_random_collide_prone_vs_oracle(ls, seed):
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(2, 400))
