@@ -332,6 +332,17 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
     __syncwarp();
 }
 
+// Segmentation of a big bucket (s > L members): up to 2L members fit one
+// buffer as a single diagonal item; bigger buckets split into n_seg balanced
+// segments of <= L members, item (I, J), J >= I, pairing segments I and J.
+__host__ __device__ __forceinline__ uint32_t n_seg(uint32_t s, uint32_t L) {
+    return s <= 2 * L ? 1u : (s + L - 1) / L;
+}
+__host__ __device__ __forceinline__ uint32_t seg_len(uint32_t s, uint32_t L) {
+    const uint32_t ns = n_seg(s, L);
+    return (s + ns - 1) / ns;
+}
+
 // chunk descriptor: x = abase | bbeg << 16; y = bend | acnt << 16 | tri << 22 | table << 23
 __device__ __forceinline__ uint2 make_chunk(uint32_t abase, uint32_t acnt, uint32_t bbeg,
                                             uint32_t bend, bool tri, uint32_t table) {
@@ -529,7 +540,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         else hi = mid;
                     }
                     bk = plan.bigb[lo];
-                    const uint64_t nseg = (bsize[bk] + L - 1) / L;
+                    const uint64_t nseg = n_seg(bsize[bk], L);
                     uint64_t rem = idx - plan.bigoff[lo], ii = 0;
                     while (rem >= nseg - ii) {
                         rem -= nseg - ii;
@@ -540,8 +551,9 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 }
                 const uint32_t s = bsize[bk];
                 const uint64_t st = bstart[bk];
-                const uint32_t i0 = I * L, nI = min(L, s - i0);
-                const uint32_t j0 = J * L, nJ = (J == I) ? 0 : min(L, s - j0);
+                const uint32_t sl = seg_len(s, L);
+                const uint32_t i0 = I * sl, nI = min(sl, s - i0);
+                const uint32_t j0 = J * sl, nJ = (J == I) ? 0 : min(sl, s - j0);
                 for (uint32_t r = lane; r < nI + nJ; r += 32)
                     cp_async4(ids + r, sids + st + (r < nI ? i0 + r : j0 + (r - nI)));
                 if (lane == 0) {
@@ -843,7 +855,7 @@ __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* _
         const uint32_t s = bsize[i];
         if (s <= L || btab[i] > tmax) continue;
         const uint64_t k = bigpos[i];
-        const uint64_t nseg = (s + L - 1) / L;
+        const uint64_t nseg = n_seg(s, L);
         bigb[k] = i;
         bigcnt[k] = nseg * (nseg + 1) / 2;
         mx = max(mx, (uint32_t)nseg);
@@ -862,7 +874,7 @@ __global__ void k_plan_bigitems(const uint32_t* __restrict__ bsize, const uint64
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nbig;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = bigb[k];
-        const uint32_t nseg = (bsize[b] + L - 1) / L;
+        const uint32_t nseg = n_seg(bsize[b], L);
         uint64_t o = bigoff[k];
         for (uint32_t I = 0; I < nseg; ++I)
             for (uint32_t J = I; J < nseg; ++J) items[o++] = (b << 24) | ((uint64_t)I << 12) | J;
