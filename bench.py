@@ -312,10 +312,16 @@ def run_ours(args):
     def step(timing=False):
         if tables_mode:
             trip, st, ds = sh.search_bits_sharded(bits, n, cfg, mapping, 0, comm=comm, timing=timing)
+            ev = None
         else:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
+            if ev:
+                ev[0].record()
             keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
+            if ev:
+                ev[1].record()
             trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=timing)
-        last.update(trip=trip, stats=st, ds=ds)
+        last.update(trip=trip, stats=st, ds=ds, sig_ev=ev)
         return ds
 
     for _ in range(max(3, args.warmup)):
@@ -326,12 +332,15 @@ def run_ours(args):
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     launches = 0
+    timed = []  # 1 GPU: per-stage CUDA events recorded inside the timed steps
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record()
         for _ in range(args.steps):
-            ds = step()
+            ds = step(timing=not tables_mode)
             launches += ds.launches + 1
+            if not tables_mode:  # events only: the step's buffers are released
+                timed.append((list(ds.events), last["sig_ev"]))
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
@@ -342,21 +351,27 @@ def run_ours(args):
     value = (n if tables_mode else world * n) / (ms / 1e3)
 
     # per-stage split + roofline of the dominant kernel (pair enumeration)
-    sig_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    sig_ev[0].record()
     if tables_mode:
+        # N > 1: one extra timed-stage search after the timed region
+        sig_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        sig_ev[0].record()
         rkeys, tags, bad = sh.gather_search_layout(bits, n, mapping, comm)
         sig_ev[1].record()
         own = sh.shard_tables(100, world, rank)
         ds = ls.DeviceSearch(sh.own_keys(rkeys, own), rkeys, tags, n, 100, timing=True, tables=own)
         trip, st, ds = sh.run_search_sharded(ds, comm, n, 100, cfg, 0)
+        torch.cuda.synchronize()
+        stages = ds.stage_times_ms()
+        stages["minhash+gather"] = sig_ev[0].elapsed_time(sig_ev[1])
     else:
-        keys, rkeys, tags, bad = ls.signatures_for_search(bits, mapping)
-        sig_ev[1].record()
-        trip, st, ds = ls.run_search(keys, rkeys, tags, n, 100, cfg, 0, timing=True)
-    torch.cuda.synchronize()
-    stages = ds.stage_times_ms()
-    stages["minhash" + ("+gather" if tables_mode else "")] = sig_ev[0].elapsed_time(sig_ev[1])
+        # 1 GPU: the stages of the K timed steps themselves (events on the
+        # launching stream), averaged
+        stages = {}
+        for evs, ev in timed:
+            for (k, ea), (_, eb) in zip(evs[:-1], evs[1:]):
+                stages[k] = stages.get(k, 0.0) + ea.elapsed_time(eb) / len(timed)
+            stages["minhash"] = stages.get("minhash", 0.0) + ev[0].elapsed_time(ev[1]) / len(timed)
+        ds, st = last["ds"], last["stats"]
     bs = ds.bsize[: ds.nb].to(torch.int64)
     hits = int((bs * (bs - 1) // 2).sum().item())
     m2 = int(bs.sum().item())
