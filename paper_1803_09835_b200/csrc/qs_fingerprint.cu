@@ -251,6 +251,23 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     return true;
 }
 
+// Shared-memory layout of k_windows (host and device agree on it).
+struct WinSmem {
+    size_t gs_off, lists_off, bytes;
+};
+__host__ __device__ inline WinSmem win_smem(uint32_t F, uint32_t T, uint32_t wmax, uint32_t nb) {
+    const size_t n = (size_t)F * T, img = n * 8, tmp = (size_t)F * wmax * 8;
+    const size_t gs = (((size_t)wmax * nb + 3) & ~(size_t)3) * 4, lists = n * 4;
+    size_t end = 2 * img + tmp;
+    WinSmem w;
+    if (gs <= img) w.gs_off = 0;
+    else { w.gs_off = end; end += gs; }
+    if (lists <= tmp) w.lists_off = 2 * img;
+    else { w.lists_off = end; end += lists; }
+    w.bytes = end + 16;
+    return w;
+}
+
 // One CTA per window (grid-stride).  mode 0: images (B,F,T) f32; 1: coeffs
 // (B,F*T) f32; 2: coeffs column-major (F*T, B) f32; 3: bits (B, K) u32.
 __global__ void __launch_bounds__(WIN_THREADS) k_windows(
@@ -262,11 +279,15 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
     const double* __restrict__ mad, void* __restrict__ out, uint32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t F = g.F, T = g.T, nb = g.nb, n = F * T;
-    double* img = (double*)smem;                       // [F*T]
-    double* hs = img + n;                              // [F*T] Haar scratch
-    double* tmp = hs + n;                              // [F*wmax]
-    float* gs = (float*)(tmp + (uint64_t)F * g.wmax);  // [wmax*nb]
-    uint16_t* lists = (uint16_t*)(gs + (((uint64_t)g.wmax * nb + 3) & ~3ull));  // [2n] top-K candidates
+    // img [n] | hs [n] Haar scratch | tmp [F*wmax] (| gs | lists when they do
+    // not fit the aliases): the band rows gs live in img until the time
+    // resample overwrites it, the top-K candidate lists in tmp after it
+    const WinSmem ly = win_smem(F, T, g.wmax, nb);
+    double* img = (double*)smem;
+    double* hs = img + n;
+    double* tmp = hs + n;
+    float* gs = (float*)(smem + ly.gs_off);
+    uint16_t* lists = (uint16_t*)(smem + ly.lists_off);
     __shared__ uint32_t hist[256];
     __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t wsum[32];
@@ -607,8 +628,7 @@ int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int
     QS_ARG(mode != 3 || (top_k >= 1 && top_k <= F * T), "bad top_k");
     if (n_win == 0) return QS_OK;
     (void)n_cols;
-    const size_t smem = (size_t)F * T * 16 + (size_t)F * wmax * 8 +
-                        (((size_t)wmax * nb + 3) & ~(size_t)3) * 4 + (size_t)F * T * 4 + 16;
+    const size_t smem = win_smem(F, T, wmax, nb).bytes;
     QS_ARG(smem <= 200 * 1024, "spectral image too large for the window kernel");
     QS_CUDA(cudaFuncSetAttribute(k_windows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     WinGeom g{n_cols, lag, win, win0, n_win, frame, hop, nb, F, T, wmin, wmax, n_levels, top_k,
