@@ -256,14 +256,14 @@ struct WinSmem {
     size_t gs_off, lists_off, bytes;
 };
 __host__ __device__ inline WinSmem win_smem(uint32_t F, uint32_t T, uint32_t wmax, uint32_t nb) {
-    const size_t n = (size_t)F * T, img = n * 8, tmp = (size_t)F * wmax * 8;
+    const size_t n = (size_t)F * T, img = n * 8, tmp = (size_t)T * nb * 8;
     const size_t gs = (((size_t)wmax * nb + 3) & ~(size_t)3) * 4, lists = n * 4;
-    size_t end = 2 * img + tmp;
+    // the third region holds the resample intermediate, later the lists
+    size_t end = 2 * img + (tmp > lists ? tmp : lists);
     WinSmem w;
+    w.lists_off = 2 * img;
     if (gs <= img) w.gs_off = 0;
     else { w.gs_off = end; end += gs; }
-    if (lists <= tmp) w.lists_off = 2 * img;
-    else { w.lists_off = end; end += lists; }
     w.bytes = end + 16;
     return w;
 }
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
     const double* __restrict__ mad, void* __restrict__ out, uint32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t F = g.F, T = g.T, nb = g.nb, n = F * T;
-    // img [n] | hs [n] Haar scratch | tmp [F*wmax] (| gs | lists when they do
+    // img [n] | hs [n] Haar scratch | tmp [T*nb] (| gs | lists when they do
     // not fit the aliases): the band rows gs live in img until the time
     // resample overwrites it, the top-K candidate lists in tmp after it
     const WinSmem ly = win_smem(F, T, g.wmax, nb);
@@ -302,23 +302,23 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < width * nb; i += blockDim.x) gs[i] = band[c0 * nb + i];
         __syncthreads();
-        // frequency resample: tmp[Fi][w] = sum_f w_f[Fi, f] * band[w][f]
-        for (uint32_t Fi = threadIdx.x >> 5; Fi < F; Fi += blockDim.x >> 5) {
-            const int32_t e0 = wf_off[Fi], e1 = wf_off[Fi + 1];
-            for (uint32_t w = threadIdx.x & 31; w < width; w += 32) {
-                double acc = 0.0;
-                for (int32_t e = e0; e < e1; ++e)
-                    acc = fma(wf_val[e], (double)gs[w * nb + wf_idx[e]], acc);
-                tmp[Fi * width + w] = acc;
-            }
+        // time resample first (the smaller intermediate): tmp[Ti][f] =
+        // sum_w w_t[Ti, w] * band[w][f]; then frequency: img[Fi][Ti] =
+        // sum_f w_f[Fi, f] * tmp[Ti][f], in f64, stored f32
+        const int32_t* to = wt_off + (uint64_t)(width - g.wmin) * (T + 1);
+        for (uint32_t i = threadIdx.x; i < T * nb; i += blockDim.x) {
+            const uint32_t Ti = udiv_u(i, nb), f = i - Ti * nb;
+            double acc = 0.0;
+            for (int32_t e = to[Ti]; e < to[Ti + 1]; ++e)
+                acc = fma(wt_val[e], (double)gs[wt_idx[e] * nb + f], acc);
+            tmp[i] = acc;
         }
         __syncthreads();
-        // time resample: img[Fi][Ti] = sum_w w_t[Ti, w] * tmp[Fi][w], stored f32
-        const int32_t* to = wt_off + (uint64_t)(width - g.wmin) * (T + 1);
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
             const uint32_t Fi = udiv_u(i, T), Ti = i - Fi * T;
             double acc = 0.0;
-            for (int32_t e = to[Ti]; e < to[Ti + 1]; ++e) acc = fma(wt_val[e], tmp[Fi * width + wt_idx[e]], acc);
+            for (int32_t e = wf_off[Fi]; e < wf_off[Fi + 1]; ++e)
+                acc = fma(wf_val[e], tmp[Ti * nb + wf_idx[e]], acc);
             img[i] = (double)(float)acc;
         }
         __syncthreads();
