@@ -23,7 +23,10 @@ namespace qs {
 
 constexpr int STFT_COLS = 128;  // columns per CTA
 constexpr int STFT_NBC = 16;    // band bins per register chunk
-constexpr int WIN_THREADS = 256;
+#ifndef QS_WIN_THREADS
+#define QS_WIN_THREADS 256
+#endif
+constexpr int WIN_THREADS = QS_WIN_THREADS;
 
 // ------------------------------------------------------------------ STFT
 // bins [b_first, b_first + nb) of a table with ld_out bins per column
