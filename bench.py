@@ -86,6 +86,36 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def cuda_core_peaks():
+    """Measured CUDA-core peaks (not in MEASURED_PEAKS.json):
+    FP64 / FP32 FMA (GFLOP/s, 2 flops per FMA) and 64-bit min/max
+    compare-selects (G/s), each the best of 3 timed launches of
+    qs_peak_launch over 148 x 32 CTAs."""
+    import ctypes
+    import torch
+    from paper_1803_09835_b200 import _native as nat
+    blocks = 148 * 32
+    scratch = torch.empty(blocks * 256 * 8, dtype=torch.uint8, device="cuda")
+    out = {}
+    for kind, name, iters, per_op in ((0, "fp64_gflops", 4096, 2.0), (1, "fp32_gflops", 16384, 2.0),
+                                      (2, "u64_minmax_gops", 8192, 1.0)):
+        ops = ctypes.c_double(0.0)
+        best = None
+        for rep in range(4):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            nat.call("qs_peak_launch", kind, blocks, iters, nat.ptr(scratch), ctypes.byref(ops),
+                     nat.stream())
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+            if rep and (best is None or ms < best):  # first launch: warm-up
+                best = ms
+        out[name] = ops.value * per_op / (best / 1e3) / 1e9
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
 
@@ -467,6 +497,25 @@ def run_ours(args):
     fpb = None
     if rank == 0 and not args.no_fingerprint:
         fpb = fingerprint_bench(args.fp_samples, max(1, args.steps), dev)
+        # the fingerprint chain against the measured FP64 peak (F_win
+        # = 74,100 flops per window + the MAD pass's rate x 68,000)
+        cpk = cuda_core_peaks()
+        fp_flops = fpb["n_fingerprints"] * (74_100 + 0.1 * 68_000)
+        fp_gf = fp_flops / (fpb["ms_per_step"] / 1e3) / 1e9
+        fpb["roofline"] = {"bound": "fp64", "achieved": fp_gf, "peak": cpk["fp64_gflops"],
+                           "peak_kind": "measured (qs_peak_launch, FP64 FMA)", "unit": "GFLOP/s",
+                           "frac": fp_gf / cpk["fp64_gflops"],
+                           "flops_per_call": fp_flops}
+        fpb["cuda_core_peaks"] = cpk
+        mh_roof = roof["other_stages"].get("minhash")
+        if mh_roof and not tables_mode:
+            # the reference kernel's work (K x t x k 64-bit compare-selects per
+            # fingerprint, _sigcore.pyx:60-75) per second of the probe kernel
+            ref_ops = 400 * 100 * 4 * n
+            rate = ref_ops / (mh_roof["ms"] / 1e3) / 1e9
+            mh_roof.update({"reference_equivalent_minmax_gops": rate,
+                            "u64_minmax_peak_gops": cpk["u64_minmax_gops"],
+                            "reference_equivalent_frac": rate / cpk["u64_minmax_gops"]})
 
     if rank == 0:
         line = {"metric": "LSH search fingerprints/sec (MinHash+bucket+pair-count)",

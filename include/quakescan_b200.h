@@ -339,6 +339,14 @@ int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len
                         uint32_t* vals_alt_dev, void* ws_dev, size_t ws_bytes,
                         int* result_in_alt, void* stream);
 
+/* CUDA-core throughput microbenchmarks for the rooflines:
+ * kind 0 FP64 FMA, 1 FP32 FMA, 2 64-bit min/max compare-select; `blocks` x
+ * 256 threads, 8 independent operations per thread and iteration;
+ * *ops_out = operations launched (time the launch with events on `stream`).
+ * scratch_dev: blocks x 256 x 8 bytes. */
+int qs_peak_launch(int kind, uint32_t blocks, uint32_t iters, void* scratch_dev,
+                   double* ops_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ SIGNATURES = {
     "qs_triplets_combine": (_int, [_p, _u64, _u32, _u32, _p, _p, _p, _sz, _p]),
     "qs_fp_pack_records": (_int, [_p, _p, _p, _u64, _u32, _p, _p]),
     "qs_fp_unpack_records": (_int, [_p, _u64, _u32, _p, _p, _p, _p]),
+    "qs_peak_launch": (_int, [_int, _u32, _u32, _p, ctypes.POINTER(ctypes.c_double), _p]),
     "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),
     "qs_radix_sort_pairs": (_int, [_p, _p, _u64, _u32, _u32, _p, _p, _p, _sz, _p, _p]),
 }
