@@ -129,23 +129,29 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* wsum, u
 // largest |v'| among eligible coefficients with ties to the lower index, bit
 // 2j + (v' < 0), ascending.  `row` is overwritten with the scores.  Returns
 // false (and writes nothing) when a coefficient is not finite.
-// Radix select over keys[i] = |v'| bits + 1 (0: ineligible), 8 bits per pass
-// from the top; after each pass only the members matching the selected
-// prefix stay on a candidate list (la / lb, ping-pong), so the later passes
-// touch a handful of coefficients.  Scratch: keys u64[n], la / lb u16[n].
+// Radix select over keys |v'| bits + 1 (0: ineligible; recomputed from the
+// scores), 8 bits per pass from the top; after each pass only the members
+// matching the selected prefix stay on a candidate list (la / lb, ping-pong),
+// so the later passes touch a handful of coefficients.  Scratch: la / lb
+// u16[n].
 __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med,
                          const double* __restrict__ mad, uint32_t top_k, uint32_t* __restrict__ ob,
                          uint32_t* hist, uint32_t* wsum, uint64_t* s_prefix, uint32_t* s_krem,
-                         uint64_t* keys, uint16_t* la, uint16_t* lb, uint32_t* s_cnt) {
+                         uint16_t* la, uint16_t* lb, uint32_t* s_cnt) {
     bool nonfinite = false;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double c = row[i];
         if (!isfinite(c)) nonfinite = true;
         const double md = mad[i];
-        const double sc = md > 0.0 ? (c - med[i]) / md : 0.0;
-        row[i] = sc;
-        keys[i] = md > 0.0 ? mag_key(sc) + 1 : 0;
+        // ineligible coefficients carry a NaN score (never selected; the
+        // reference's 0 score is never output for them)
+        row[i] = md > 0.0 ? (c - med[i]) / md : __longlong_as_double(0x7FF8000000000000ll);
     }
+    // select key of coefficient i: |v'| bits + 1, 0 when ineligible
+    auto key_of = [&](uint32_t i) -> uint64_t {
+        const double v = row[i];
+        return v != v ? 0ull : mag_key(v) + 1;
+    };
     for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     if (threadIdx.x == 0) {
         *s_prefix = 0;
@@ -155,7 +161,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     if (__syncthreads_or(nonfinite)) return false;
     // pass 0: histogram of the top byte over all eligible coefficients
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint64_t k = keys[i];
+        const uint64_t k = key_of(i);
         if (k) atomicAdd(&hist[k >> 56], 1u);
     }
     uint16_t* cur = la;
@@ -205,7 +211,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
         const uint32_t lim = shift == 56 ? n : ncur;
         for (uint32_t j = threadIdx.x; j < lim; j += blockDim.x) {
             const uint32_t i = shift == 56 ? j : cur[j];
-            const uint64_t k = keys[i];
+            const uint64_t k = key_of(i);
             if (k && ((uint32_t)(k >> shift) & 0xFFu) == dsel) {
                 nxt[atomicAdd(&s_cnt[1], 1u)] = (uint16_t)i;
                 atomicAdd(&hist[(k >> (shift - 8)) & 0xFF], 1u);
@@ -223,7 +229,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     const uint32_t i0 = min(n, threadIdx.x * per), i1 = min(n, i0 + per);
     uint32_t gt = 0, eq = 0;
     for (uint32_t i = i0; i < i1; ++i) {
-        const uint64_t k = keys[i];
+        const uint64_t k = key_of(i);
         gt += k > thr;
         eq += k == thr;
     }
@@ -233,7 +239,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     const uint32_t eq_before = block_scan_u32(eq, wsum, nullptr);
     uint32_t sel = 0, eqr = eq_before;
     for (uint32_t i = i0; i < i1; ++i) {
-        const uint64_t k = keys[i];
+        const uint64_t k = key_of(i);
         if (k > thr) ++sel;
         else if (k == thr) {
             if (eqr < need) ++sel;
@@ -243,7 +249,7 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     uint32_t pos = block_scan_u32(sel, wsum, nullptr);
     eqr = eq_before;
     for (uint32_t i = i0; i < i1; ++i) {
-        const uint64_t k = keys[i];
+        const uint64_t k = key_of(i);
         bool take = k > thr;
         if (k == thr) {
             take = eqr < need;
@@ -254,19 +260,25 @@ __device__ bool topk_row(double* row, uint32_t n, const double* __restrict__ med
     return true;
 }
 
-// Shared-memory layout of k_windows (host and device agree on it).
+// Shared-memory layout of k_windows (host and device agree on it): img [n]
+// f64 | hs [n] f64.  hs is the Haar scratch; before the Haar it holds the
+// time-resample intermediate (T x nb f64), after it the top-K candidate
+// lists (2n u16).  The band rows (wmax x nb f32) live in img until the
+// frequency resample overwrites it.  Anything that does not fit its alias
+// gets its own region after hs.
 struct WinSmem {
-    size_t gs_off, lists_off, bytes;
+    size_t tmp_off, gs_off, lists_off, bytes;
 };
 __host__ __device__ inline WinSmem win_smem(uint32_t F, uint32_t T, uint32_t wmax, uint32_t nb) {
     const size_t n = (size_t)F * T, img = n * 8, tmp = (size_t)T * nb * 8;
     const size_t gs = (((size_t)wmax * nb + 3) & ~(size_t)3) * 4, lists = n * 4;
-    // the third region holds the resample intermediate, later the lists
-    size_t end = 2 * img + (tmp > lists ? tmp : lists);
+    size_t end = 2 * img;
     WinSmem w;
-    w.lists_off = 2 * img;
+    if (tmp <= img) w.tmp_off = img;
+    else { w.tmp_off = end; end += tmp; }
     if (gs <= img) w.gs_off = 0;
     else { w.gs_off = end; end += gs; }
+    w.lists_off = img;  // lists <= hs always (4n <= 8n bytes)
     w.bytes = end + 16;
     return w;
 }
@@ -282,13 +294,11 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
     const double* __restrict__ mad, void* __restrict__ out, uint32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t F = g.F, T = g.T, nb = g.nb, n = F * T;
-    // img [n] | hs [n] Haar scratch | tmp [T*nb] (| gs | lists when they do
-    // not fit the aliases): the band rows gs live in img until the time
-    // resample overwrites it, the top-K candidate lists in tmp after it
+    // layout: see WinSmem (resample scratch and top-K lists alias hs)
     const WinSmem ly = win_smem(F, T, g.wmax, nb);
     double* img = (double*)smem;
     double* hs = img + n;
-    double* tmp = hs + n;
+    double* tmp = (double*)(smem + ly.tmp_off);
     float* gs = (float*)(smem + ly.gs_off);
     uint16_t* lists = (uint16_t*)(smem + ly.lists_off);
     __shared__ uint32_t hist[256];
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
         }
         // ---- mode 3: scores, K-th largest |score| (radix select), bits
         if (!topk_row(img, n, med, mad, g.top_k, (uint32_t*)out + wi * g.top_k, hist, wsum,
-                      &s_prefix, &s_krem, (uint64_t*)hs, lists, lists + n, s_cnt))
+                      &s_prefix, &s_krem, lists, lists + n, s_cnt))
             if (threadIdx.x == 0) atomicOr(flags, 1u);
     }
 }
@@ -468,8 +478,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_topk_rows(const TC* __restrict_
                                                            uint32_t* __restrict__ flags) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* row = (double*)smem;
-    uint64_t* keys = (uint64_t*)(row + n);
-    uint16_t* lists = (uint16_t*)(keys + n);
+    uint16_t* lists = (uint16_t*)(row + n);
     __shared__ uint32_t hist[256];
     __shared__ uint32_t wsum[32];
     __shared__ uint64_t s_prefix;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(WIN_THREADS) k_topk_rows(const TC* __restrict_
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) row[i] = (double)c[r * n + i];
         __syncthreads();
         if (!topk_row(row, n, med, mad, top_k, out + r * top_k, hist, wsum, &s_prefix, &s_krem,
-                      keys, lists, lists + n, s_cnt))
+                      lists, lists + n, s_cnt))
             if (threadIdx.x == 0) atomicOr(flags, 1u);
     }
 }
@@ -669,7 +678,7 @@ int qs_fp_topk_bits(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
                     uint32_t* flags_dev, void* stream) {
     QS_ARG(top_k >= 1 && top_k <= n, "top_k must be in [1, n]");
     if (B == 0) return QS_OK;
-    const size_t smem = (size_t)n * 20;  // row f64 + keys u64 + two u16 candidate lists
+    const size_t smem = (size_t)n * 12;  // row f64 + two u16 candidate lists
     QS_ARG(smem <= 200 * 1024, "coefficient rows too long");
     const unsigned grid = (unsigned)(B < 148 * 32 ? B : 148 * 32);
     cudaStream_t st = (cudaStream_t)stream;
