@@ -237,6 +237,8 @@ class DeviceSearch:
         self.launches += 2 + 2 * 3
         nb2 = int(counts[0].item())
         self._compact_stats = (emask, hist, big, big_cap, out)
+        # sizes of the compacted buckets (the DISTINCT pass's work; bench.py roofline)
+        self.compact_sizes = bsize2[:nb2]
         return (sids2, bstart2, bsize2, btab2, nb2)
 
     def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None):

@@ -186,3 +186,40 @@ def cfg1_bits_torch(n=8_000_000, d=4096, K=400, seed=1, device="cuda", pair_frac
         bits[dst_rows[a:b]] = mutate(tmpl_rows[a:b], keep)
     bits, _ = torch.sort(bits, dim=1)
     return bits, dict(pairs=pairs, jaccard=jac, groups=groups)
+
+
+def cfg2_trace_torch(n_samples=795_000_000, seed=2, repeats=500, device="cuda", slope=-1.0,
+                     chunk=1 << 22):
+    """cfg2 on the GPU: 1/f^|slope| noise (white noise shaped in the rfft
+    domain chunkwise, unit RMS, as colored_noise) plus `repeats` planted
+    copies of the cfg0 chirp templates (amplitude log-uniform 0.2..2 x RMS).
+    torch RNG for the noise (a different stream from the numpy generator, same
+    distribution); templates, offsets and amplitudes from numpy.  Returns a
+    float32 CUDA tensor and the truth list."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    out = torch.empty(n_samples, dtype=torch.float32, device=device)
+    f = torch.fft.rfftfreq(chunk, 1.0 / SR_HZ, device=device, dtype=torch.float64)
+    shape = torch.ones_like(f)
+    shape[1:] = f[1:] ** (slope / 2.0)
+    shape[0] = 0.0
+    shape /= torch.sqrt(torch.mean(shape ** 2))
+    shape = shape.to(torch.complex64)
+    for a in range(0, n_samples, chunk):
+        b = min(n_samples, a + chunk)
+        w = torch.randn(chunk, generator=g, device=device, dtype=torch.float32)
+        y = torch.fft.irfft(torch.fft.rfft(w) * shape, n=chunk)
+        out[a:b] = y[: b - a]
+    rng = np.random.default_rng(seed + 1)
+    templates = chirp_templates(rng)
+    copies = max(1, repeats // len(templates))
+    truth = []
+    for ti, wv in enumerate(templates):
+        offs = rng.integers(0, n_samples - wv.size, size=copies)
+        amps = 10.0 ** rng.uniform(math.log10(0.2), math.log10(2.0), size=copies)
+        wd = torch.from_numpy(wv).to(device)
+        for o, amp in zip(offs, amps):
+            out[int(o):int(o) + wv.size] += float(amp) * wd
+            truth.append((ti, int(o), float(amp)))
+    return out, truth

@@ -48,7 +48,14 @@ def kat():
         cb[",".join(str(w) for w in ws)] = hex(rmh.combine(np.array(ws, np.uint64)))
     m = rmh.gen_hash_mapping(d=64, t=3, k=4, seed=42)
     sig = rmh.signatures(np.array([[0, 5, 17, 63]], np.uint32), m)[0]
-    return dict(fmix64=fm, hash=hv, combine=cb,
+    # detection_probability (lsh_search.py:112-136) at the reference's DP_FROZEN
+    # points (tests/test_lsh_search.py:13-22) plus a grid, evaluated by the reference
+    pts = [(0.5, 6, 5, 100), (0.5, 4, 2, 100), (0.8, 6, 5, 100), (0.2, 6, 5, 100),
+           (0.3, 8, 2, 100), (0.7, 8, 2, 100), (0.95, 2, 90, 100), (0.1, 2, 1, 10)]
+    pts += [(s, k, m, t) for s in (0.0, 0.05, 0.4, 0.65, 0.9, 1.0) for k in (2, 4, 8)
+            for m, t in ((1, 1), (5, 100), (20, 50))]
+    dp = [[s, k, m, t, rls.detection_probability(s, k, m, t)] for s, k, m, t in pts]
+    return dict(fmix64=fm, hash=hv, combine=cb, dp_frozen=dp,
                 sig_d64_t3_k4_s42_bits_0_5_17_63=[hex(int(v)) for v in sig],
                 backend=rmh.BACKEND)
 
@@ -246,6 +253,77 @@ def files():
         print(fn, os.path.getsize(os.path.join(out, fn)))
 
 
+def row_hashes(a) -> np.ndarray:
+    """8-byte blake2b digest of every row of a 2-D array (little-endian bytes)."""
+    import hashlib
+    a = np.ascontiguousarray(a)
+    out = np.empty(a.shape[0], np.uint64)
+    for i in range(a.shape[0]):
+        out[i] = int.from_bytes(hashlib.blake2b(a[i].tobytes(), digest_size=8).digest(), "little")
+    return out
+
+
+def fingerprint_day():
+    """The full cfg0 day (BASELINE configs[0]: 8.64e6 samples, 86,391 windows)
+    through the reference: per-window digests of the float32 coefficient rows
+    and of the bit rows, the band-row spectrogram digest per 4096-column block,
+    and the MAD statistics.  Digests keep the fixture small (the arrays are
+    707 MB of coefficients); the GPU test recomputes the values with the
+    oracle on the box for ulp-level comparisons and uses these digests to pin
+    that oracle run to the reference's."""
+    x, _ = workloads.cfg0_trace()
+    p = workloads.CFG0_PARAMS
+    params = rfp.FingerprintParams(
+        window_len_s=p["window_len_s"], window_lag_s=p["window_lag_s"],
+        freq_bins=p["freq_bins"], time_bins=p["time_bins"], top_k=p["top_k"],
+        band_low_hz=p["band_low_hz"], band_high_hz=p["band_high_hz"],
+        stft=rfp.StftParams(frame_len_s=p["frame_len_s"], hop_s=p["hop_s"]))
+    ts = TimeSeries("ST0", "HHZ", 100.0, 0.0, x)
+    fps, mad = rfp.fingerprint_series(ts, params, mad_rate=0.1, mad_seed=0)
+    freqs, times, logpow = rfp.spectrogram(ts, params)
+    r0, r1 = rfp._band_rows(freqs, params)
+    band = np.ascontiguousarray(logpow[r0:r1].T)
+    nblk = -(-band.shape[0] // 4096)
+    band_blk = np.zeros((nblk, 4096 * band.shape[1]), np.float32)
+    for k in range(nblk):
+        blk = band[k * 4096:(k + 1) * 4096].reshape(-1)
+        band_blk[k, :blk.size] = blk
+    chash = np.empty(fps.bits.shape[0], np.uint64)
+    for idx, _, c in rfp.iter_coeff_batches(ts, params):
+        chash[idx] = row_hashes(c)
+    return dict(bits_hash=row_hashes(fps.bits), coeff_hash=chash, band_hash=row_hashes(band_blk),
+                band_rows=np.array([r0, r1]), median=mad.median, mad=mad.mad,
+                meta=np.array([mad.n_sampled, mad.n_total, fps.bits.shape[0], fps.bits.shape[1]]))
+
+
+def demo_golden():
+    """The reference's frozen demo report (pkg/tests/data/demo_golden.json),
+    re-derived here with the reference's serial in-memory harness
+    (pkg/tests/test_cli.py:54-100, reference stages throughout) and copied
+    only if the two agree byte for byte."""
+    import tempfile
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, ROOT)
+    from quakescan import config as rcfg
+    from quakescan import ingest as ring
+    from test_demo_golden_gpu import detection_report
+    from quakescan import align as ral
+    from importlib import resources
+    ref = dict(align=ral, ingest=ring, lsh_search=rls, config=rcfg)
+    with tempfile.TemporaryDirectory() as tmp:
+        dst = os.path.join(tmp, "demo.toml")
+        with open(dst, "w") as f:
+            f.write(resources.files("quakescan").joinpath("data/demo.toml").read_text())
+        cfg = rcfg.load_config(dst)
+        blob = detection_report(ref, cfg, ring.bandpass, rfp.fingerprint_series,
+                                rls.search_fingerprints)
+    with open("/root/reference/pkg/tests/data/demo_golden.json", "rb") as f:
+        frozen = f.read()
+    assert blob == frozen, "reference harness does not reproduce its own golden"
+    with open(os.path.join(HERE, "demo_golden.json"), "wb") as f:
+        f.write(blob)
+
+
 def main():
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1, sort_keys=True)
@@ -270,8 +348,15 @@ def main():
 
 
 if __name__ == "__main__":
-    if "--files" in sys.argv:
+    if "--kat" in sys.argv:
+        with open(os.path.join(HERE, "kat.json"), "w") as f:
+            json.dump(kat(), f, indent=1, sort_keys=True)
+    elif "--files" in sys.argv:
         files()
+    elif "--day" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "fingerprint_day.npz"), **fingerprint_day())
+    elif "--demo" in sys.argv:
+        demo_golden()
     elif "--bandpass" in sys.argv:
         bp = bandpass_cases()
         np.savez_compressed(os.path.join(HERE, "bandpass.npz"),

@@ -1,8 +1,10 @@
 """Fingerprint chain parity on the GPU.
 
-Tolerances (north star): spectrogram and wavelet values within 1e-4 relative
-(with an absolute floor of 1e-4 * max|ref| for near-zero detail
-coefficients); binary fingerprints agree on >= 99.9% of bits.  Mirrors the
+Tolerances are set at what the f64 design delivers (measured, see
+tests/test_fingerprint_day.py), far inside the north star's 1e-4 relative /
+99.9 % of bits: spectrogram and image values within 1 float32 ulp,
+coefficients within 1 ulp of their window's largest magnitude, MAD
+statistics to 1e-12 relative, fingerprint bits identical.  Mirrors the
 reference's tests/test_fingerprint.py strategy (Haar oracle + roundtrip,
 resize constants, top-K oracle with ties and sign encoding, MAD definition,
 error taxonomy) plus golden vectors produced by the reference itself."""
@@ -16,7 +18,7 @@ from oracle import fingerprint as ofp
 
 pytestmark = pytest.mark.gpu
 
-RTOL = 1e-4
+ULP = 1
 
 
 @pytest.fixture(scope="module")
@@ -33,11 +35,19 @@ def _params(fp, p):
                                 stft=fp.StftParams(p["frame_len_s"], p["hop_s"]))
 
 
-def _close(got, want):
-    got = np.asarray(got, np.float64)
-    want = np.asarray(want, np.float64)
-    atol = RTOL * max(1.0, float(np.abs(want).max()))
-    np.testing.assert_allclose(got, want, rtol=RTOL, atol=atol)
+def _close(got, want, per_row=False):
+    """|got - want| <= ULP float32 ulps of want (elementwise), or of the row's
+    largest magnitude (per_row: Haar detail coefficients near zero)."""
+    got = np.asarray(got, np.float32).astype(np.float64)
+    want = np.asarray(want, np.float32)
+    if per_row:
+        w2 = want.reshape(want.shape[0], -1)
+        scale = np.abs(w2).max(axis=1, keepdims=True).astype(np.float32)
+        ulp = np.broadcast_to(np.spacing(scale), w2.shape).reshape(want.shape)
+    else:
+        ulp = np.spacing(np.abs(want))
+    err = np.abs(got - want.astype(np.float64))
+    assert np.all(err <= ULP * ulp.astype(np.float64)), float((err / ulp).max())
 
 
 def _ts(x, sr=100.0, start=0.0):
@@ -54,19 +64,19 @@ def test_golden_cfg0_chain(fp, golden_fingerprint):
     r0, r1 = (int(v) for v in case["band_rows"])
     _close(logpow[r0:r1].T, case["band"])
     exact = np.mean(logpow[r0:r1].T == case["band"])
-    assert exact > 0.999
+    assert exact > 0.9999
     (idx, ep, imgs), = list(fp.iter_image_batches(ts, params, indices=case["sel"]))
     _close(imgs, case["images"])
     (idx, ep, coeffs), = list(fp.iter_coeff_batches(ts, params, indices=case["sel"]))
-    _close(coeffs, case["coeffs"])
+    _close(coeffs, case["coeffs"], per_row=True)
     assert np.array_equal(idx, case["sel"]) and np.allclose(ep, 1000.0 + case["sel"] * 1.0)
     fps, mad = fp.fingerprint_series(ts, params, mad_rate=0.1, mad_seed=0)
     assert (mad.n_sampled, mad.n_total) == tuple(int(v) for v in case["meta"])
-    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-5, atol=1e-7)
-    np.testing.assert_allclose(mad.mad, case["mad"], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(mad.mad, case["mad"], rtol=1e-12, atol=0)
     assert np.array_equal(mad.mad > 0, case["mad"] > 0)  # the structural zero-MAD coefficients
     assert fps.bits.shape == case["bits"].shape and fps.bits.dtype == np.uint32
-    assert np.mean(fps.bits == case["bits"]) >= 0.999
+    assert np.array_equal(fps.bits, case["bits"])
     fps.validate()
     assert fps.meta["station"] == "ST0" and fps.d == 4096
 
@@ -76,8 +86,8 @@ def test_golden_small_full_band(fp, golden_fingerprint):
     params = fp.FingerprintParams(window_len_s=3.0, window_lag_s=0.5, freq_bins=8, time_bins=12,
                                   top_k=24, stft=fp.StftParams(frame_len_s=0.5, hop_s=0.05))
     fps, mad = fp.fingerprint_series(_ts(case["samples"]), params, mad_rate=1.0)
-    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-5, atol=1e-7)
-    assert np.mean(fps.bits == case["bits"]) >= 0.999
+    np.testing.assert_allclose(mad.median, case["median"], rtol=1e-12, atol=0)
+    assert np.array_equal(fps.bits, case["bits"])
 
 
 def test_random_traces_vs_oracle(fp):
@@ -91,8 +101,10 @@ def test_random_traces_vs_oracle(fp):
         x = rng.standard_normal(n)  # float64 trace
         res = ofp.fingerprint(x, 100.0, params, mad_rate=0.5, mad_seed=3)
         fps, mad = fp.fingerprint_series(_ts(x), _params(fp, params), mad_rate=0.5, mad_seed=3)
-        np.testing.assert_allclose(mad.median, res["median"], rtol=1e-5, atol=1e-7)
-        assert np.mean(fps.bits == res["bits"]) >= 0.999
+        np.testing.assert_allclose(mad.median, res["median"], rtol=1e-9, atol=1e-12)
+        agree = float(np.mean(fps.bits == res["bits"]))
+        print(f"random trace n={n}: bits agreement {agree:.6f}")
+        assert agree >= 0.9999
 
 
 def test_haar_matches_oracle_and_roundtrip(fp):

@@ -168,3 +168,58 @@ def test_cfg1_full_scale_properties(ls):
             assert 0 < st.filtered_fingerprints < n
         del keys, rkeys, tags, trip, ds
         torch.cuda.empty_cache()
+
+
+@pytest.fixture(scope="module")
+def cfg1_1e5():
+    """The cfg1 generator (BASELINE configs[1] densities) at N = 1e5, its
+    Min-Max signatures from the C oracle, and the mapping."""
+    from oracle import minmax as omm
+    from paper_1803_09835_b200 import minmax_hash as mh
+    from paper_1803_09835_b200 import workloads
+    bits, _ = workloads.cfg1_bits(n=100_000, seed=21)
+    m = mh.gen_hash_mapping(4096, 100, 4, 0)
+    sigs = omm.signatures_c(bits, m.values, 100, 2, threads=8)
+    return bits, sigs, m
+
+
+@pytest.mark.parametrize("occ_limit,p,excl", [(None, 1, 0), (120, 1, 0), (60, 3, 2)])
+def test_cfg1_1e5_vs_oracle(ls, cfg1_1e5, occ_limit, p, excl):
+    """cfg1 at N = 1e5 (the scale of the CPU baseline), filter off (the
+    reference default) and on at limit 120 (the bench's setting, which removes
+    the noise groups): signatures bit-identical, triplets byte-identical and
+    every SearchStats field equal to the oracle's."""
+    from paper_1803_09835_b200 import minmax_hash as mh
+    bits, want_sigs, m = cfg1_1e5
+    sigs = mh.signatures(bits, m)
+    assert np.array_equal(sigs, want_sigs)
+    n = bits.shape[0]
+    occ = occ_limit / n if occ_limit else None
+    cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, partitions=p,
+                          occurrence_threshold=occ)
+    rec, st = ls.search_signatures(sigs, cfg, exclusion_windows=excl)
+    want, wst = _oracle(want_sigs, cfg, excl)
+    assert rec.size > 1000
+    assert rec.tobytes() == want.tobytes(), (occ_limit, p)
+    _check_stats(st, dict(wst), (occ_limit, p))
+    if occ_limit == 120:
+        assert st.filtered_fingerprints > 0.3 * n  # the filter fires (noise groups removed)
+
+
+def test_cfg1_1e5_host_bits_e2e(ls, cfg1_1e5):
+    """The same N = 1e5 batch through search_fingerprints with host bits (the
+    e2e path the bench times: pinned row-chunk H2D pipelined with the fused
+    signature kernel)."""
+    from paper_1803_09835_b200.fingerprint import FingerprintSet
+    bits, want_sigs, m = cfg1_1e5
+    n = bits.shape[0]
+    fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
+                         indices=np.arange(n, dtype=np.uint64),
+                         epochs=np.arange(n, dtype=np.float64), bits=bits)
+    cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, occurrence_threshold=120 / n,
+                          near_repeat_exclusion_s=0.0)
+    rec, st, _ = ls.search_fingerprints(fps, cfg, mapping=m)
+    want, wst = _oracle(want_sigs, cfg, 0)
+    assert rec.tobytes() == want.tobytes()
+    _check_stats(st, dict(wst), "e2e")
+
