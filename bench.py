@@ -398,9 +398,7 @@ def pair_roofline(ds, stages, n_trip, m, t, hbm, peak_kind, filt):
     removed); FULL walks every bucket."""
     import torch
     bs = ds.bsize[: ds.nb].to(torch.int64)
-    bt = ds.btab[: ds.nb]
-    if ds.table_ids is not None:
-        bt = ds.table_ids[bt.long()]
+    bt = ds.btab[: ds.nb]  # global table ids (a sharded rank's listing maps them)
     passes = {}
 
     def acc(sizes):

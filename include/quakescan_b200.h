@@ -33,6 +33,8 @@ extern "C" {
 #define QS_ERR_OOM 2   /* device allocation failed             -> MemoryError    */
 #define QS_ERR_CUDA 3  /* CUDA runtime / launch failure        -> RuntimeError   */
 #define QS_ERR_DATA 4  /* input data unusable (e.g. bit >= d)  -> DataError      */
+#define QS_ERR_CAPACITY 5 /* caller's output capacity too small; *needed_out holds
+                             the count to size it for (re-call with that)  */
 
 /* ---------------------------------------------------------------- library */
 const char* qs_version(void);
@@ -260,6 +262,58 @@ size_t qs_triplets_combine_ws_bytes(uint64_t n);
 int qs_triplets_combine(const uint8_t* triplets_dev, uint64_t n, uint32_t threshold,
                         uint32_t key_bits, uint8_t* out_dev, uint64_t* count_dev, void* ws_dev,
                         size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- one-call search entries
+ * The whole search in one call for non-Python callers: the same stage
+ * sequence the Python host layer runs (lsh_search.py run_search), every
+ * buffer carved from ONE caller workspace (no cudaMalloc inside), the stream
+ * synchronised only where a count sizes the next stage.  Results are
+ * identical to the stage-by-stage path and to the reference. */
+
+/* SearchStats (lsh_search.py:70-109); lookups_per_query and selectivity are
+ * derived (lookups_total / n_queries, 2 * distinct_pairs / n^2). */
+typedef struct qs_search_stats {
+    uint64_t n_fingerprints;
+    uint64_t n_queries;
+    uint64_t lookups_total;
+    uint64_t distinct_pairs;
+    uint64_t emitted_triplets;
+    uint64_t filtered_fingerprints;
+    uint64_t peak_table_entries;
+    uint64_t n_buckets;
+    uint64_t max_bucket;
+    double top_bucket_mass;
+    uint32_t n_partitions;  /* len(partition_bounds(n, partitions)) */
+} qs_search_stats;
+
+/* search_signatures(sigs, SearchConfig(tables=t, min_matches=m,
+ * partitions=partitions, occurrence_threshold=occurrence_threshold or None
+ * when <= 0), exclusion_windows) (lsh_search.py:222-303).  sigs_dev (n, t)
+ * uint64 row-major; triplets_dev receives the emitted TRIPLET_DTYPE records
+ * (20 B each, sorted by (dt, idx1)), stats->emitted_triplets of them.
+ * pair_cap bounds the matched pairs of an enumeration pass (and the output):
+ * QS_ERR_CAPACITY with *needed_out = the pairs found when it is too small.
+ * Workspace: qs_lsh_search_ws_bytes(n, t, pair_cap, partitions). */
+size_t qs_lsh_search_ws_bytes(uint64_t n, uint32_t t, uint64_t pair_cap, uint32_t partitions);
+int qs_lsh_search(const uint64_t* sigs_dev, uint64_t n, uint32_t t, uint32_t m,
+                  uint64_t exclusion_windows, double occurrence_threshold, uint32_t partitions,
+                  uint8_t* triplets_dev, uint64_t pair_cap, uint64_t* needed_out,
+                  qs_search_stats* stats, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* search_fingerprints(fps, cfg, mapping=None) (lsh_search.py:314-333) from
+ * set-bit indices bits_dev (n, K) uint32: the hash mapping
+ * gen_hash_mapping(d, t, 2 * k_half, seed) and its probe plan are built in the
+ * workspace, signatures go straight into the search layout, then the search
+ * as qs_lsh_search.  A bit index >= d -> QS_ERR_ARG (ParameterError).
+ * Workspace: qs_lsh_search_bits_ws_bytes(n, d, t, k_half, pair_cap, partitions). */
+size_t qs_lsh_search_bits_ws_bytes(uint64_t n, uint32_t d, uint32_t t, uint32_t k_half,
+                                   uint64_t pair_cap, uint32_t partitions);
+int qs_lsh_search_bits(const uint32_t* bits_dev, uint64_t n, uint32_t K, uint32_t d,
+                       uint64_t seed, uint32_t t, uint32_t k_half, uint32_t m,
+                       uint64_t exclusion_windows, double occurrence_threshold,
+                       uint32_t partitions, uint8_t* triplets_dev, uint64_t pair_cap,
+                       uint64_t* needed_out, qs_search_stats* stats, void* ws_dev,
+                       size_t ws_bytes, void* stream);
 
 /* Zero-phase band-pass (scipy.signal.sosfiltfilt with padtype "odd", as
  * reference ingest.py:74-84 calls it): sos_host (n_sections x 6, a0 == 1) and

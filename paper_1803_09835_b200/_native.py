@@ -14,7 +14,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # QS_LIB_PATH: an alternative build of the same library (kernel-configuration sweeps)
 LIB_PATH = os.environ.get("QS_LIB_PATH") or os.path.join(HERE, "lib", "libquakescan_b200.so")
 
-QS_OK, QS_ERR_ARG, QS_ERR_OOM, QS_ERR_CUDA, QS_ERR_DATA = 0, 1, 2, 3, 4
+QS_OK, QS_ERR_ARG, QS_ERR_OOM, QS_ERR_CUDA, QS_ERR_DATA, QS_ERR_CAPACITY = 0, 1, 2, 3, 4, 5
+
+
+class SearchStatsC(ctypes.Structure):
+    """struct qs_search_stats (include/quakescan_b200.h)."""
+    _fields_ = [("n_fingerprints", ctypes.c_uint64), ("n_queries", ctypes.c_uint64),
+                ("lookups_total", ctypes.c_uint64), ("distinct_pairs", ctypes.c_uint64),
+                ("emitted_triplets", ctypes.c_uint64), ("filtered_fingerprints", ctypes.c_uint64),
+                ("peak_table_entries", ctypes.c_uint64), ("n_buckets", ctypes.c_uint64),
+                ("max_bucket", ctypes.c_uint64), ("top_bucket_mass", ctypes.c_double),
+                ("n_partitions", ctypes.c_uint32)]
 
 _u8p = ctypes.c_void_p
 _p = ctypes.c_void_p
@@ -79,6 +89,13 @@ SIGNATURES = {
     "qs_fp_pack_records": (_int, [_p, _p, _p, _u64, _u32, _p, _p]),
     "qs_fp_unpack_records": (_int, [_p, _u64, _u32, _p, _p, _p, _p]),
     "qs_peak_launch": (_int, [_int, _u32, _u32, _p, ctypes.POINTER(ctypes.c_double), _p]),
+    "qs_lsh_search_ws_bytes": (_sz, [_u64, _u32, _u64, _u32]),
+    "qs_lsh_search": (_int, [_p, _u64, _u32, _u32, _u64, _dbl, _u32, _p, _u64,
+                             ctypes.POINTER(_u64), ctypes.POINTER(SearchStatsC), _p, _sz, _p]),
+    "qs_lsh_search_bits_ws_bytes": (_sz, [_u64, _u32, _u32, _u32, _u64, _u32]),
+    "qs_lsh_search_bits": (_int, [_p, _u64, _u32, _u32, _u64, _u32, _u32, _u32, _u64, _dbl, _u32,
+                                  _p, _u64, ctypes.POINTER(_u64), ctypes.POINTER(SearchStatsC), _p,
+                                  _sz, _p]),
     "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),
     "qs_radix_sort_pairs": (_int, [_p, _p, _u64, _u32, _u32, _p, _p, _p, _sz, _p, _p]),
 }
