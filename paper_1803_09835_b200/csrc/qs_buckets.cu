@@ -12,6 +12,8 @@
 // members scattered in one pass, each bin sorted in shared memory by id-rank
 // + key sub-bin counting — came to 56 ms against the radix path's 50 ms: the
 // per-bin sort is instruction-bound (~30 warp instructions per member).
+#include <stdlib.h>
+
 #include "qs_lsh.cuh"
 
 namespace qs {
@@ -138,7 +140,14 @@ using namespace qs;
 
 extern "C" {
 
+// QS_BUCKET_RADIX=1 selects the round-1 LSD radix build (A/B measurements)
+static bool use_radix_build() {
+    const char* e = getenv("QS_BUCKET_RADIX");
+    return e && e[0] == '1';
+}
+
 size_t qs_lsh_bucket_flags_ws_bytes(uint64_t n, uint32_t t) {
+    if (!use_radix_build()) return bucket_bins_ws_bytes(n, t);
     // sorted keys + the radix build's own workspace
     return (size_t)n * t * 8 + 256 + qs_lsh_bucket_ws_bytes(n, t);
 }
@@ -149,6 +158,8 @@ int qs_lsh_build_bucket_flags(const uint64_t* keys_dev, uint64_t n, uint32_t t,
     cudaStream_t st = (cudaStream_t)stream;
     if (n == 0 || t == 0) return QS_OK;
     QS_ARG(ws_bytes >= qs_lsh_bucket_flags_ws_bytes(n, t), "bucket workspace too small");
+    if (!use_radix_build())
+        return bucket_bins_build(keys_dev, n, t, ids_out_dev, flags_out_dev, ws_dev, ws_bytes, st);
     const uint64_t total = n * t;
     uint64_t* skeys = (uint64_t*)ws_dev;
     void* rws = (void*)(((uintptr_t)(skeys + total) + 255) & ~(uintptr_t)255);

@@ -21,6 +21,11 @@ int num_sms();
 int make_bucket_sizes(const uint64_t* bstart, const uint64_t* counts, uint64_t n, uint32_t* bsize,
                       uint32_t* btab, const uint32_t* table_ids, cudaStream_t st);
 
+// bucket build by key-range bins + shared-memory bin sorts (qs_bucket_bins.cu)
+size_t bucket_bins_ws_bytes(uint64_t n, uint32_t t);
+int bucket_bins_build(const uint64_t* keys, uint64_t n, uint32_t t, uint32_t* sids, uint8_t* flags,
+                      void* ws, size_t ws_bytes, cudaStream_t st);
+
 __device__ __forceinline__ uint64_t mix_key(uint64_t s) { return fmix64(s ^ GOLDEN64); }
 
 // partition index of fingerprint i: edges[k] <= i < edges[k+1]

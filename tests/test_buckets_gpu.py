@@ -94,6 +94,34 @@ def test_prefix_collisions_keep_full_key_order():
     assert np.array_equal(flags, want_flags)
 
 
+@pytest.mark.parametrize("big", [6_000, 15_000, 40_000])
+def test_bins_with_one_huge_bucket(big):
+    """A bucket bigger than the shared-memory bin sort (mid: 4k-16k members,
+    giant: > 16k) next to ordinary keys, plus 32-bit prefix collisions."""
+    rng = np.random.default_rng(big)
+    n, t = 300_000, 2
+    keys = _mix(rng.integers(0, 2**40, size=(t, n)).astype(np.uint64))
+    pos = rng.choice(n, big, replace=False)
+    keys[0, pos] = keys[0, 0]
+    keys[1, pos[: big // 2]] = keys[1, 7]
+    # same top 32 bits as the huge bucket's key, different low bits
+    keys[0, rng.choice(n, 50, replace=False)] = (keys[0, 0] & ~np.uint64(0xFFFFFFFF)) | np.uint64(5)
+    want_ids, want_flags = _expected(keys)
+    ids, flags = _build(keys)
+    assert np.array_equal(ids, want_ids)
+    assert np.array_equal(flags, want_flags)
+
+
+def test_large_table_many_bins():
+    rng = np.random.default_rng(9)
+    n, t = 3_000_000, 2
+    keys = _mix(rng.integers(0, 400_000, size=(t, n)).astype(np.uint64))
+    want_ids, want_flags = _expected(keys)
+    ids, flags = _build(keys)
+    assert np.array_equal(ids, want_ids)
+    assert np.array_equal(flags, want_flags)
+
+
 def test_all_identical_keys():
     n, t = 20_000, 2
     keys = np.full((t, n), 12345, np.uint64)
