@@ -376,6 +376,44 @@ int qs_fp_haar2d(double* data_dev, uint64_t B, uint32_t H, uint32_t W, const int
 int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const double* med_dev,
                     const double* mad_dev, double* out_dev, void* stream);
 
+/* Fingerprint geometry (FingerprintParams + StftParams, fingerprint.py:44-88).
+ * band_low_hz <= 0 and band_high_hz <= 0: the full band. */
+typedef struct qs_fp_params {
+    double window_len_s;
+    double window_lag_s;
+    uint32_t freq_bins;
+    uint32_t time_bins;
+    uint32_t top_k;
+    double band_low_hz;
+    double band_high_hz;
+    double frame_len_s;
+    double hop_s;
+} qs_fp_params;
+
+/* n_windows (fingerprint.py:189-195) after the same validation as
+ * FingerprintParams.validate; QS_ERR_DATA for a series shorter than one window. */
+int qs_fp_n_windows(uint64_t n_samples, double sample_rate_hz, const qs_fp_params* params,
+                    uint64_t* n_windows_out);
+
+/* fingerprint_series (fingerprint.py:581-623) in one call: band STFT, the MAD
+ * pass over the windows mad_sample_dev[0 .. n_mad_sample) (sorted int64
+ * window indices — the reference draws them with numpy's
+ * default_rng(mad_seed).choice, fingerprint.py:356-362) writing med_dev /
+ * mad_dev (n_coeffs float64 each), then the top_k sign bits of every window
+ * into bits_dev (n_windows, top_k) uint32.  mad_sample_dev == NULL: med_dev /
+ * mad_dev are inputs (fingerprint_series(stats=...)).  x_dev: float64 samples,
+ * or float32 with x_is_f32 (widened exactly).  Errors as the reference:
+ * ParameterError (QS_ERR_ARG) for geometry / top_k > eligible coefficients,
+ * DataError (QS_ERR_DATA) for short series or non-finite coefficients.
+ * Synchronises the stream twice (eligible count, non-finite flag). */
+size_t qs_fingerprint_chain_ws_bytes(uint64_t n_samples, double sample_rate_hz,
+                                     const qs_fp_params* params, uint64_t n_mad_sample);
+int qs_fingerprint_chain(const void* x_dev, int x_is_f32, uint64_t n_samples,
+                         double sample_rate_hz, const qs_fp_params* params,
+                         const int64_t* mad_sample_dev, uint64_t n_mad_sample, double* med_dev,
+                         double* mad_dev, uint32_t* bits_dev, uint64_t* n_windows_out, void* ws_dev,
+                         size_t ws_bytes, void* stream);
+
 /* .fp file records (fingerprint.py:529-551 layout: index u64 | epoch f64 |
  * bits u32[K], little endian, 16 + 4K bytes each) packed from / unpacked to
  * device columns, so fingerprint files stream through one D2H / H2D copy. */

@@ -17,6 +17,15 @@ LIB_PATH = os.environ.get("QS_LIB_PATH") or os.path.join(HERE, "lib", "libquakes
 QS_OK, QS_ERR_ARG, QS_ERR_OOM, QS_ERR_CUDA, QS_ERR_DATA, QS_ERR_CAPACITY = 0, 1, 2, 3, 4, 5
 
 
+class FpParamsC(ctypes.Structure):
+    """struct qs_fp_params (include/quakescan_b200.h)."""
+    _fields_ = [("window_len_s", ctypes.c_double), ("window_lag_s", ctypes.c_double),
+                ("freq_bins", ctypes.c_uint32), ("time_bins", ctypes.c_uint32),
+                ("top_k", ctypes.c_uint32), ("band_low_hz", ctypes.c_double),
+                ("band_high_hz", ctypes.c_double), ("frame_len_s", ctypes.c_double),
+                ("hop_s", ctypes.c_double)]
+
+
 class SearchStatsC(ctypes.Structure):
     """struct qs_search_stats (include/quakescan_b200.h)."""
     _fields_ = [("n_fingerprints", ctypes.c_uint64), ("n_queries", ctypes.c_uint64),
@@ -96,6 +105,10 @@ SIGNATURES = {
     "qs_lsh_search_bits": (_int, [_p, _u64, _u32, _u32, _u64, _u32, _u32, _u32, _u64, _dbl, _u32,
                                   _p, _u64, ctypes.POINTER(_u64), ctypes.POINTER(SearchStatsC), _p,
                                   _sz, _p]),
+    "qs_fp_n_windows": (_int, [_u64, _dbl, ctypes.POINTER(FpParamsC), ctypes.POINTER(_u64)]),
+    "qs_fingerprint_chain_ws_bytes": (_sz, [_u64, _dbl, ctypes.POINTER(FpParamsC), _u64]),
+    "qs_fingerprint_chain": (_int, [_p, _int, _u64, _dbl, ctypes.POINTER(FpParamsC), _p, _u64, _p,
+                                    _p, _p, ctypes.POINTER(_u64), _p, _sz, _p]),
     "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),
     "qs_radix_sort_pairs": (_int, [_p, _p, _u64, _u32, _u32, _p, _p, _p, _sz, _p, _p]),
 }

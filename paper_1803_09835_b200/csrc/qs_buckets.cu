@@ -140,10 +140,13 @@ using namespace qs;
 
 extern "C" {
 
-// QS_BUCKET_RADIX=1 selects the round-1 LSD radix build (A/B measurements)
+// QS_BUCKET_BINS=1 selects the two-pass build of qs_bucket_bins.cu (2 radix
+// passes + shared-memory range sorts): 81 instead of 143 B per (member,
+// table) but measured 32-36 ms against this path's 31.7 ms at cfg1 — the
+// range sorts are latency-bound
 static bool use_radix_build() {
-    const char* e = getenv("QS_BUCKET_RADIX");
-    return e && e[0] == '1';
+    const char* e = getenv("QS_BUCKET_BINS");
+    return !(e && e[0] == '1');
 }
 
 size_t qs_lsh_bucket_flags_ws_bytes(uint64_t n, uint32_t t) {

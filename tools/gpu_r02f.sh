@@ -1,0 +1,10 @@
+#!/bin/bash
+# bucket build v2 (2 radix passes + range sorts): parity + A/B timing; C fingerprint chain tests
+cd "$GRAFT_REPO_ROOT"
+timeout 900 python -m pytest tests/test_buckets_gpu.py tests/test_capi_fingerprint_gpu.py -q -x -p no:cacheprovider > gpurun_out/r02f_buckets.log 2>&1
+echo "buckets rc=$?" >> gpurun_out/r02f_buckets.log
+timeout 1200 python -m pytest tests/test_lsh_gpu.py tests/test_capi_search_gpu.py tests/test_sharded_gpu.py -q -x -p no:cacheprovider > gpurun_out/r02f_lsh.log 2>&1
+echo "lsh rc=$?" >> gpurun_out/r02f_lsh.log
+B='python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-fingerprint --no-e2e --full-steps 0'
+timeout 600 $B > gpurun_out/r02f_bench_bins.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_bb_|k_rs_" -c 12 python tools/one_search.py > gpurun_out/r02f_ncu_bb.log 2>&1
