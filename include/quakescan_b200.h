@@ -93,7 +93,11 @@ int qs_minmax_signatures_search_rows(const uint32_t* bits_dev, uint64_t n, uint6
  * `_core.gen_signatures_range(bits, values, t, k_half, out, start, stop)`
  * (minmax_hash.py:24-30 selects it; _sigcore.pyx:32-36 defines it): fills
  * out[start:stop] (n_rows, t) from bits (n_rows, K) and values (d, F).
- * Stages through device memory on an internal stream; synchronous. */
+ * Stages through device memory on an internal stream; synchronous.  The
+ * stream, device buffers and the uploaded mapping + probe plan persist
+ * across calls (the reference calls once per worker chunk with one mapping):
+ * the mapping is re-uploaded when its address, shape or a strided digest of
+ * its values changes.  Calls are serialised internally (thread-safe). */
 int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
                             const uint64_t* values, uint32_t d, uint32_t F,
                             int32_t t, int32_t k_half, uint64_t* out,
@@ -372,9 +376,11 @@ int qs_fp_topk_bits(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
 int qs_fp_haar2d(double* data_dev, uint64_t B, uint32_t H, uint32_t W, const int32_t* sched_dev,
                  uint32_t n_levels, int inverse, void* stream);
 
-/* normalize (fingerprint.py:425-430): (c - median)/MAD, 0 where MAD == 0. */
-int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const double* med_dev,
-                    const double* mad_dev, double* out_dev, void* stream);
+/* normalize (fingerprint.py:425-430): (c - median)/MAD in float64, 0 where
+ * MAD == 0; B rows of n coefficients, float32 or float64 (is_f64).  med_dev /
+ * mad_dev hold n values. */
+int qs_fp_normalize(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
+                    const double* med_dev, const double* mad_dev, double* out_dev, void* stream);
 
 /* Fingerprint geometry (FingerprintParams + StftParams, fingerprint.py:44-88).
  * band_low_hz <= 0 and band_high_hz <= 0: the full band. */

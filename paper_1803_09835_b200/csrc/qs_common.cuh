@@ -38,6 +38,24 @@ int cuda_status(cudaError_t e, const char* what);
 
 }  // namespace qs
 
+// Debug builds (make EXTRA=-DQS_DEBUG_CHECKS, the sanitizer substitute of
+// DESIGN.md §3): device-side bounds assertions on the shared-memory and global
+// indices of the asynchronous kernels; a failure traps the kernel.
+#ifdef QS_DEBUG_CHECKS
+#define QS_DASSERT(c)                                                                   \
+    do {                                                                                \
+        if (!(c)) {                                                                     \
+            printf("QS_DASSERT %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,      \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                              \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define QS_DASSERT(c) \
+    do {              \
+    } while (0)
+#endif
+
 #define QS_CHECK_LAUNCH(what)                                              \
     do {                                                                   \
         cudaError_t _e = cudaGetLastError();                               \

@@ -458,7 +458,8 @@ __global__ void k_mid_mean(const double* __restrict__ a, const double* __restric
     if (i < n) out[i] = (a[i] + b[i]) / 2.0;  // np.median of an even count
 }
 
-__global__ void k_normalize(const float* __restrict__ c, uint64_t total, uint32_t n,
+template <typename TC>
+__global__ void k_normalize(const TC* __restrict__ c, uint64_t total, uint32_t n,
                             const double* __restrict__ med, const double* __restrict__ mad,
                             double* __restrict__ out) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -708,11 +709,16 @@ int qs_fp_haar2d(double* data_dev, uint64_t B, uint32_t H, uint32_t W, const int
     return QS_OK;
 }
 
-int qs_fp_normalize(const float* coeffs_dev, uint64_t B, uint32_t n, const double* med_dev,
-                    const double* mad_dev, double* out_dev, void* stream) {
+int qs_fp_normalize(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,
+                    const double* med_dev, const double* mad_dev, double* out_dev, void* stream) {
     if (B == 0) return QS_OK;
-    k_normalize<<<qs_blocks(B * n, 256), 256, 0, (cudaStream_t)stream>>>(coeffs_dev, B * n, n, med_dev,
-                                                                         mad_dev, out_dev);
+    const unsigned g = qs_blocks(B * n, 256);
+    if (is_f64)
+        k_normalize<double><<<g, 256, 0, (cudaStream_t)stream>>>((const double*)coeffs_dev, B * n, n,
+                                                                 med_dev, mad_dev, out_dev);
+    else
+        k_normalize<float><<<g, 256, 0, (cudaStream_t)stream>>>((const float*)coeffs_dev, B * n, n,
+                                                                med_dev, mad_dev, out_dev);
     QS_CHECK_LAUNCH("k_normalize");
     return QS_OK;
 }

@@ -11,6 +11,8 @@
 // bits set the expected number of probes per column is d/K (≈10 at cfg1)
 // instead of K compare-selects (400): the same outputs, bit for bit, because
 // the plan is built from the mapping values themselves (ties share a value).
+#include <mutex>
+
 #include "qs_common.cuh"
 
 namespace qs {
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256) k_signatures(
                     h |= ((bm[xb >> 5] >> (xb & 31)) & 1u) << (2 * e + 1);
                 }
                 r += 8;
+                QS_DASSERT(seq < 2 * F);
                 if (h || r >= d) {  // r >= d only when every bit was invalid
                     rk[seq] = h ? (uint16_t)(r - 8 + __ffs(h) - 1) : (uint16_t)0;
                     seq += 32;
@@ -232,6 +235,102 @@ static size_t sig_smem_per_warp(uint32_t d, uint32_t F) {
     return ((words * 4 + 15) & ~15u) + (((size_t)2 * F * 2 + 15) & ~(size_t)15);
 }
 
+
+// Plan-free Min-Max for d > PLAN_MAX_D (the probe plan's u16 element order and
+// shared-memory sort stop there): the reference's own loop (_sigcore.pyx:60-75)
+// — per row, elementwise min/max of the mapping rows of its K set bits, one
+// warp per row, lanes over hash columns (coalesced 8-byte loads of a mapping
+// row), then the same fold and search-layout epilogue as k_signatures.
+template <bool SEARCH>
+__global__ void __launch_bounds__(128) k_signatures_direct(
+    const uint32_t* __restrict__ bits, uint64_t n, uint32_t K, const uint64_t* __restrict__ values,
+    uint32_t d, uint32_t F, uint32_t t, uint32_t kh, uint64_t* __restrict__ sigs,
+    uint64_t* __restrict__ keys, uint64_t* __restrict__ rkeys, uint32_t* __restrict__ tags,
+    uint32_t* __restrict__ bad, uint64_t row_lo, uint64_t row_hi) {
+    extern __shared__ __align__(16) uint64_t dsm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* mn = dsm + (uint64_t)warp * 2 * F;
+    uint64_t* mx = mn + F;
+    const uint32_t W = (t + 31) >> 5;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t row = row_lo + blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp; row < row_hi;
+         row += nw) {
+        const uint32_t* br = bits + row * K;
+        bool badrow = false;
+        for (uint32_t f0 = 0; f0 < F; f0 += 32) {
+            const uint32_t f = f0 + lane;
+            uint64_t lo = ~0ull, hi = 0;
+            for (uint32_t k = 0; k < K; ++k) {
+                uint32_t x = __ldg(br + k);
+                if (x >= d) {
+                    badrow = true;
+                    x = 0;
+                }
+                if (f < F) {
+                    const uint64_t v = __ldg(values + (uint64_t)x * F + f);
+                    lo = v < lo ? v : lo;
+                    hi = v > hi ? v : hi;
+                }
+            }
+            if (f < F) {
+                mn[f] = lo;
+                mx[f] = hi;
+            }
+        }
+        if (__any_sync(0xffffffffu, badrow) && lane == 0) atomicExch(bad, 1u);
+        __syncwarp();
+        for (uint32_t wr = 0; wr < W; ++wr) {
+            const uint32_t i = wr * 32 + lane;
+            uint64_t acc = 0;
+            if (i < t) {
+                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mn[i * kh + j]);
+                for (uint32_t j = 0; j < kh; ++j) acc = combine1(acc, mx[i * kh + j]);
+                if (sigs) sigs[row * t + i] = acc;
+            }
+            if (SEARCH) {
+                const uint64_t key = mix_key(acc);
+                if (i < t) {
+                    if (keys) keys[(uint64_t)i * n + row] = key;
+                    rkeys[row * t + i] = key;
+                }
+                const uint32_t tag = (uint32_t)key & 0xFFFFu;
+                uint32_t plane = 0;
+#pragma unroll
+                for (int b = 0; b < 16; ++b) {
+                    uint32_t word = __ballot_sync(0xffffffffu, (i < t) && ((tag >> b) & 1u));
+                    if (lane == (uint32_t)b) plane = word;
+                }
+                if (lane < 16) tags[((uint64_t)(lane >> 3) * n + row) * W * 8 + wr * 8 + (lane & 7)] = plane;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+static int launch_direct(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
+                         const uint64_t* values, uint32_t d, uint32_t t, uint32_t kh,
+                         uint64_t* sigs, uint64_t* keys, uint64_t* rkeys, uint32_t* tags,
+                         uint32_t* bad, cudaStream_t st, uint64_t row0, uint64_t nrows) {
+    const uint32_t F = t * kh;
+    const size_t smem = (size_t)4 * 2 * F * 8;
+    QS_ARG(smem <= 200 * 1024, "t*k too large for the signature kernel (F=%u)", F);
+    const unsigned grid = qs_blocks((nrows + 3) / 4, 1, 148 * 16);
+    if (search) {
+        QS_CUDA(cudaFuncSetAttribute(k_signatures_direct<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+        k_signatures_direct<true><<<grid, 128, smem, st>>>(bits, n, K, values, d, F, t, kh, sigs, keys,
+                                                           rkeys, tags, bad, row0, row0 + nrows);
+    } else {
+        QS_CUDA(cudaFuncSetAttribute(k_signatures_direct<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+        k_signatures_direct<false><<<grid, 128, smem, st>>>(bits, n, K, values, d, F, t, kh, sigs,
+                                                            nullptr, nullptr, nullptr, bad, row0,
+                                                            row0 + nrows);
+    }
+    QS_CHECK_LAUNCH("k_signatures_direct");
+    return QS_OK;
+}
+
 static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint32_t K,
                              const void* plan, uint32_t d, uint32_t t, uint32_t kh,
                              uint64_t* sigs, uint64_t* keys, uint64_t* rkeys, uint32_t* tags,
@@ -240,9 +339,12 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
     if (nrows == ~0ull) nrows = n - row0;
     QS_ARG(row0 <= n && nrows <= n - row0, "row range out of bounds");
     QS_ARG(K >= 1, "fingerprints must have at least one set bit");
-    QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
+    QS_ARG(d >= 1, "d must be >= 1");
     QS_ARG(t >= 1 && kh >= 1, "t and k/2 must be >= 1");
     if (nrows == 0) return QS_OK;
+    if (d > PLAN_MAX_D)  // the "plan" is a copy of the mapping values (qs_minmax_plan)
+        return launch_direct(search, bits, n, K, (const uint64_t*)plan, d, t, kh, sigs, keys,
+                             rkeys, tags, bad, st, row0, nrows);
     const uint32_t F = t * kh;
     const uint16_t* order = (const uint16_t*)plan;
     const uint64_t* svals = (const uint64_t*)((const unsigned char*)plan + plan_order_bytes(d, F));
@@ -285,6 +387,45 @@ static int launch_signatures(bool search, const uint32_t* bits, uint64_t n, uint
 
 using namespace qs;
 
+
+// persistent state of qs_gen_signatures_range (host plugin entry)
+struct GsrCtx {
+    int dev = -1;
+    cudaStream_t st = nullptr;
+    uint64_t *dv = nullptr, *dout = nullptr;
+    uint32_t *dbits = nullptr, *dbad = nullptr;
+    void* plan = nullptr;
+    size_t dv_cap = 0, plan_cap = 0, dbits_cap = 0, dout_cap = 0, dbad_cap = 0;
+    const uint64_t* key_values = nullptr;
+    uint32_t key_d = 0, key_F = 0;
+    uint64_t key_digest = 0;
+    int ensure(void** p, size_t* cap, size_t bytes) {
+        if (*cap >= bytes && *p) return QS_OK;
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+        *cap = 0;
+        const cudaError_t e = cudaMalloc(p, bytes);
+        if (e != cudaSuccess) return qs::cuda_status(e, "cudaMalloc");
+        *cap = bytes;
+        if (p == (void**)&dv || p == &plan) key_values = nullptr;  // contents lost
+        return QS_OK;
+    }
+    void release() {
+        if (st) cudaStreamDestroy(st);
+        for (void* q : {(void*)dv, (void*)dout, (void*)dbits, (void*)dbad, plan})
+            if (q) cudaFree(q);
+        *this = GsrCtx();
+    }
+};
+
+// digest of a mapping: its shape plus every 97th value (the mapping is
+// generated, never edited in place; a different array gets a new upload)
+static uint64_t values_digest(const uint64_t* v, uint64_t count) {
+    uint64_t h = count * 0x9E3779B97F4A7C15ULL;
+    for (uint64_t i = 0; i < count; i += 97) h = qs::fmix64(h ^ v[i]);
+    return qs::fmix64(h ^ v[count - 1]);
+}
+
 extern "C" {
 
 int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs, uint64_t seed,
@@ -297,13 +438,19 @@ int qs_gen_hash_mapping(uint64_t* values_dev, uint32_t d, uint32_t n_funcs, uint
 }
 
 size_t qs_minmax_plan_bytes(uint32_t d, uint32_t n_funcs) {
+    if (d > PLAN_MAX_D) return (size_t)d * n_funcs * 8;  // plan-free path: the values themselves
     return plan_blk_offset(d, n_funcs) + (size_t)2 * n_funcs * PLAN_BLK * sizeof(uint16_t);
 }
 
 int qs_minmax_plan(const uint64_t* values_dev, uint32_t d, uint32_t n_funcs, void* plan_dev,
                    void* stream) {
-    QS_ARG(d >= 1 && d <= PLAN_MAX_D, "d=%u outside the supported range [1, %u]", d, PLAN_MAX_D);
+    QS_ARG(d >= 1, "d must be >= 1");
     QS_ARG(n_funcs >= 1, "n_funcs must be >= 1");
+    if (d > PLAN_MAX_D) {  // plan-free (direct) signatures read the values
+        QS_CUDA(cudaMemcpyAsync(plan_dev, values_dev, (size_t)d * n_funcs * 8,
+                                cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "copy values");
+        return QS_OK;
+    }
     uint32_t dpad = 1;
     while (dpad < d) dpad <<= 1;
     if (dpad < 2) dpad = 2;
@@ -354,44 +501,58 @@ int qs_gen_signatures_range(const uint32_t* bits, uint64_t n_rows, uint32_t K,
     QS_ARG(K >= 1, "fingerprints must have at least one set bit");
     QS_ARG(start <= stop && stop <= n_rows, "row range out of bounds");
     if (stop == start) return QS_OK;
-    cudaStream_t st;
-    QS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    // The reference calls this once per worker chunk with the same mapping
+    // (minmax_hash.py:113-128): the stream, the device buffers and the
+    // uploaded mapping + probe plan persist across calls (keyed by the
+    // mapping's address, shape and a strided digest of its values); calls
+    // are serialised by a mutex (the device serialises them anyway).
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static GsrCtx ctx;
+    int dev = 0;
+    QS_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    if (ctx.st == nullptr || ctx.dev != dev) {
+        ctx.release();
+        ctx.dev = dev;
+        QS_CUDA(cudaStreamCreateWithFlags(&ctx.st, cudaStreamNonBlocking), "stream");
+    }
+    cudaStream_t st = ctx.st;
     const uint64_t rows = stop - start;
     const uint64_t chunk = rows < (1u << 20) ? rows : (1u << 20);
-    uint64_t *dv = nullptr, *dout = nullptr;
-    uint32_t *dbits = nullptr, *dbad = nullptr;
-    void* plan = nullptr;
+    const size_t vb = (size_t)d * F * 8, pb = qs_minmax_plan_bytes(d, F);
     int rc = QS_OK;
-    cudaError_t e = cudaSuccess;
-    size_t pb = qs_minmax_plan_bytes(d, F);
-    if ((e = cudaMallocAsync((void**)&dv, (size_t)d * F * 8, st)) != cudaSuccess ||
-        (e = cudaMallocAsync(&plan, pb, st)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&dbits, chunk * K * 4, st)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&dout, chunk * (uint64_t)t * 8, st)) != cudaSuccess ||
-        (e = cudaMallocAsync((void**)&dbad, 4, st)) != cudaSuccess) {
-        rc = cuda_status(e, "cudaMallocAsync");
+    if ((rc = ctx.ensure((void**)&ctx.dv, &ctx.dv_cap, vb)) ||
+        (rc = ctx.ensure(&ctx.plan, &ctx.plan_cap, pb)) ||
+        (rc = ctx.ensure((void**)&ctx.dbits, &ctx.dbits_cap, chunk * K * 4)) ||
+        (rc = ctx.ensure((void**)&ctx.dout, &ctx.dout_cap, chunk * (uint64_t)t * 8)) ||
+        (rc = ctx.ensure((void**)&ctx.dbad, &ctx.dbad_cap, 4)))
+        return rc;
+    const uint64_t digest = values_digest(values, (uint64_t)d * F);
+    if (!(ctx.key_values == values && ctx.key_d == d && ctx.key_F == F && ctx.key_digest == digest)) {
+        QS_CUDA(cudaMemcpyAsync(ctx.dv, values, vb, cudaMemcpyHostToDevice, st), "H2D mapping");
+        rc = qs_minmax_plan(ctx.dv, d, F, ctx.plan, st);
+        if (rc) {
+            ctx.key_values = nullptr;
+            return rc;
+        }
+        ctx.key_values = values;
+        ctx.key_d = d;
+        ctx.key_F = F;
+        ctx.key_digest = digest;
     }
-    if (rc == QS_OK) {
-        cudaMemcpyAsync(dv, values, (size_t)d * F * 8, cudaMemcpyHostToDevice, st);
-        cudaMemsetAsync(dbad, 0, 4, st);
-        rc = qs_minmax_plan(dv, d, F, plan, st);
-    }
+    QS_CUDA(cudaMemsetAsync(ctx.dbad, 0, 4, st), "memset");
     for (uint64_t a = start; rc == QS_OK && a < stop; a += chunk) {
         uint64_t m = (stop - a) < chunk ? (stop - a) : chunk;
-        cudaMemcpyAsync(dbits, bits + a * K, m * K * 4, cudaMemcpyHostToDevice, st);
-        rc = qs_minmax_signatures(dbits, m, K, plan, d, (uint32_t)t, (uint32_t)k_half, dout, dbad, st);
+        QS_CUDA(cudaMemcpyAsync(ctx.dbits, bits + a * K, m * K * 4, cudaMemcpyHostToDevice, st), "H2D");
+        rc = qs_minmax_signatures(ctx.dbits, m, K, ctx.plan, d, (uint32_t)t, (uint32_t)k_half,
+                                  ctx.dout, ctx.dbad, st);
         if (rc == QS_OK)
-            cudaMemcpyAsync(out + a * t, dout, m * (uint64_t)t * 8, cudaMemcpyDeviceToHost, st);
+            QS_CUDA(cudaMemcpyAsync(out + a * t, ctx.dout, m * (uint64_t)t * 8,
+                                    cudaMemcpyDeviceToHost, st), "D2H");
     }
     uint32_t hbad = 0;
-    if (rc == QS_OK) cudaMemcpyAsync(&hbad, dbad, 4, cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(dv, st);
-    cudaFreeAsync(plan, st);
-    cudaFreeAsync(dbits, st);
-    cudaFreeAsync(dout, st);
-    cudaFreeAsync(dbad, st);
-    e = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    if (rc == QS_OK) QS_CUDA(cudaMemcpyAsync(&hbad, ctx.dbad, 4, cudaMemcpyDeviceToHost, st), "D2H");
+    const cudaError_t e = cudaStreamSynchronize(st);
     if (rc == QS_OK && e != cudaSuccess) rc = cuda_status(e, "qs_gen_signatures_range");
     if (rc == QS_OK && hbad) {
         set_error("fingerprint bit index out of range for mapping");

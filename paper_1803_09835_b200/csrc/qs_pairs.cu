@@ -169,6 +169,22 @@ __device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
                      (uint32_t)__cvta_generic_to_shared(bar))
                  : "memory");
 }
+// expect `bytes` of bulk-copy transactions on the barrier and arrive once
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// TMA-engine bulk copy global -> shared (16-byte aligned, size % 16 == 0),
+// completion counted on the barrier's transaction count
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
     uint32_t done = 0;
@@ -281,7 +297,9 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
                                       unsigned long long& distinct) {
     if (lane < cnt) {
         const uint32_t e = (base + lane) & (QCAP - 1);
+        QS_DASSERT(e < QCAP);
         const uint32_t a = q.qa[e], b = q.qb[e], f = q.qt[e];
+        QS_DASSERT(a < b);
         const uint32_t table = (f & 0xFFu) | ((f >> 16) << 8);
         const int wt = (int)(table >> 5);
         const uint32_t bt = table & 31, low = (1u << bt) - 1u;
@@ -372,6 +390,7 @@ __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, ui
     for (uint32_t c = 0; c * 32 < s; ++c) {
         const uint32_t ab = off + c * 32, acnt = min(32u, s - c * 32);
         if (fold && acnt >= 2) chunks[base++] = make_chunk(ab, acnt, 0, 0, true, table);
+        QS_DASSERT(acnt >= 1 && acnt <= 32);
         const uint32_t first = fold ? acnt : 1;
         const uint32_t np = n_pieces(c * 32 + first, s);
         for (uint32_t k = 0; k < np; ++k) {
@@ -384,6 +403,7 @@ __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, ui
 template <int W, class Lay, int ROWP>
 __device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const uint32_t* __restrict__ tags,
                                           uint64_t n, uint32_t id, uint32_t wg) {
+    QS_DASSERT(id < n);
     uint4* dst = (uint4*)(rows + pos * ROWP);
 #pragma unroll
     for (int w = 0; w < W; ++w)
@@ -405,7 +425,7 @@ struct Plan {
                                  // [4] max segments per bucket, [5] item table valid
 };
 
-template <int W, int MODE, bool HAS_E, int WT>
+template <int W, int MODE, bool HAS_E, int WT, bool EX>
 __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_pc(
     const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
     const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab, Plan plan,
@@ -500,6 +520,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         const uint32_t s = (uint32_t)(mp1 - mp0);
                         const uint32_t kk = nsb + __popc(bal & lt);
                         const uint32_t off = (uint32_t)(mp0 - mbase);
+                        QS_DASSERT(kk < L);
                         p_off[kk] = off;
                         p_st[kk] = __ldg(bstart + b0 + i);
                         const uint32_t cb = atomicAdd(&s_nch[ma], count_chunks_tri(s, FOLD));
@@ -518,6 +539,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         if (p_off[mid] <= r) lo = mid;
                         else hi = mid;
                     }
+                    QS_DASSERT(r < C::CAP && lo < nsb);
                     cp_async4(ids + r, sids + p_st[lo] + (r - p_off[lo]));
                 }
                 cp_async_wait_all();
@@ -554,8 +576,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 const uint32_t sl = seg_len(s, L);
                 const uint32_t i0 = I * sl, nI = min(sl, s - i0);
                 const uint32_t j0 = J * sl, nJ = (J == I) ? 0 : min(sl, s - j0);
-                for (uint32_t r = lane; r < nI + nJ; r += 32)
+                for (uint32_t r = lane; r < nI + nJ; r += 32) {
+                    QS_DASSERT(r < C::CAP);
                     cp_async4(ids + r, sids + st + (r < nI ? i0 + r : j0 + (r - nI)));
+                }
                 if (lane == 0) {
                     const uint32_t table = btab[bk];
                     uint32_t cbase = 0;
@@ -587,8 +611,14 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
             if (k >= NBUF) mbar_wait(&empty_bar[b], ((k / NBUF) - 1) & 1);
             PROF_STOP(0)
             PROF_START
+            // MATCHED rows are the first plane group of every word, contiguous in
+            // `tags` ([2][n][W][8]): one TMA bulk copy per row, completion on the
+            // barrier's transaction count; the other modes gather planes of
+            // some words (per-thread 16-byte cp.async)
+            const bool bulk = MODE == MODE_MATCHED && (uint32_t)W == wg;
             if (s_nch[ma] == NCH_DONE) {
-                mbar_arrive_cp_async(&full_bar[b]);
+                if (bulk) mbar_arrive(&full_bar[b]);
+                else mbar_arrive_cp_async(&full_bar[b]);
                 mbar_arrive(&full_bar[b]);
                 break;
             }
@@ -596,11 +626,22 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 uint32_t* rows = rowsb(b);
                 const uint32_t* ids = idsm(ma);
                 const uint32_t nrows = s_nrows[ma];
-                for (uint32_t r = lane; r < nrows; r += 32) stage_row<W, Lay, C::ROWP>(rows, r, tags, n, ids[r], wg);
+                if (bulk) {
+                    constexpr uint32_t RB = (uint32_t)C::ROW * 4;
+                    const uint32_t mine = nrows > lane ? (nrows - lane + 31) / 32 : 0;
+                    mbar_arrive_expect_tx(&full_bar[b], mine * RB);
+                    for (uint32_t r = lane; r < nrows; r += 32) {
+                        QS_DASSERT(r < C::CAP && ids[r] < n);
+                        bulk_g2s(rows + r * C::ROWP, tags + (uint64_t)ids[r] * wg * 8, RB, &full_bar[b]);
+                    }
+                } else {
+                    for (uint32_t r = lane; r < nrows; r += 32)
+                        stage_row<W, Lay, C::ROWP>(rows, r, tags, n, ids[r], wg);
+                }
             }
             __syncwarp();
-            mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
-            mbar_arrive(&full_bar[b]);           // releases the descriptor of item k
+            if (!bulk) mbar_arrive_cp_async(&full_bar[b]);  // fires when this lane's row copies land
+            mbar_arrive(&full_bar[b]);                       // releases the descriptor of item k
             // look ahead: the descriptor area of item k + NPROD belonged to item
             // k + NPROD - NMETA = k - NBUF, released by the empty wait above
             stage_meta((k + NPROD) % C::NMETA);
@@ -645,6 +686,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
             if (lane == 0) ci = atomicAdd(&s_next[msel], 1u);
             ci = __shfl_sync(0xffffffffu, ci, 0);
             if (ci >= nch) break;
+            QS_DASSERT(ci < C::MAXCH);
             const uint2 d = chunks[ci];
             const uint32_t abase = d.x & 0xFFFFu, bbeg = d.x >> 16;
             const uint32_t bend = d.y & 0xFFFFu, acnt = (d.y >> 16) & 63u;
@@ -674,7 +716,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 a_ok = emask[a] == 0;
                 a_part = p > 1 ? part_of(edges, p, a) : 0;
             }
-            const bool excl_on = excl > 0;
+            constexpr bool excl_on = EX;  // exclusion windows (excl > 0) at compile time
             // evaluate the pair (a, row u): validity, tag-plane masks, queue decision.
             // Rectangular chunks: row u lies after every A row (its id is larger).
             // Fold chunks: row u may precede the lane's row, so the pair is taken
@@ -687,7 +729,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     if (excl_on || HAS_E) {
                         const uint32_t bid = ids[u];
                         const uint32_t c = min(a, bid), qv = max(a, bid);
-                        valid = valid && (uint64_t)(qv - c) > excl;
+                        if (excl_on) valid = valid && (uint64_t)(qv - c) > excl;
                         if (HAS_E && valid) {
                             if (emask[c]) valid = false;
                             else if (emask[qv] && (p <= 1 || part_of(edges, p, qv) ==
@@ -699,7 +741,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     valid = a_ok && u >= (tri ? apos + 1 : bbeg);  // tri: pairs j > i
                     if (excl_on || HAS_E) {
                         const uint32_t bid = ids[u];
-                        valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend within a bucket
+                        if (excl_on) valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend in a bucket
                         if (HAS_E && valid && emask[bid] &&
                             (p <= 1 || part_of(edges, p, bid) == a_part))
                             valid = false;
@@ -770,8 +812,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
                         const uint32_t bid = ids[u];
-                        q.qa[e] = fold ? min(a, bid) : a;
-                        q.qb[e] = fold ? max(a, bid) : bid;
+                        const uint32_t qa = fold ? min(a, bid) : a, qb = fold ? max(a, bid) : bid;
+                        QS_DASSERT(e < QCAP && qa < qb && qb < n);
+                        q.qa[e] = qa;
+                        q.qb[e] = qb;
                         q.qt[e] = flags;
 #pragma unroll
                         for (int w = 0; w < W; ++w) q.qm[e * W + w] = qmask[w];
@@ -1032,7 +1076,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
     QS_CHECK_LAUNCH("plan");
     Plan plan{mpre, tile_first, items, bigb, bigoff, totals};
-    auto kern = k_pairs_pc<W, MODE, HAS_E, WT>;
+    auto kern = excl > 0 ? k_pairs_pc<W, MODE, HAS_E, WT, true> : k_pairs_pc<W, MODE, HAS_E, WT, false>;
     QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM),
             "smem attr");
     int per_sm = 1;

@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(RS_THREADS, QS_RS_MINB) k_rs_scatter(
         if (i < seg_len) {
             const uint32_t dgt = (uint32_t)((k[r] >> shift) & 0xFF);
             const uint32_t lp = dstart[dgt] + wcnt[warp][dgt] + rank[r];
+            QS_DASSERT(lp < tile_n);
             sk[lp] = k[r];
             sv[lp] = v[r];
         }
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(RS_THREADS, QS_RS_MINB) k_rs_scatter(
         const uint64_t key = sk[j];
         const uint32_t dgt = (uint32_t)((key >> shift) & 0xFF);
         const uint64_t pos = base + goff[dgt] + (j - dstart[dgt]);
+        QS_DASSERT(pos < base + seg_len && j >= dstart[dgt]);
         okeys[pos] = key;
         ovals[pos] = sv[j];
     }

@@ -427,17 +427,24 @@ def estimate_mad(ts, params: FingerprintParams, rate: float = 0.1, seed: int = 0
 
 
 def normalize(coeffs, stats: MadStats) -> np.ndarray:
-    """Deviation scores v' = (v - median) / MAD; zero-MAD columns give 0 (fingerprint.py:425-430)."""
+    """Deviation scores v' = (v - median) / MAD in float64; zero-MAD columns
+    give 0 (fingerprint.py:425-430).  float32 rows (the chain's coefficients)
+    are read as float32, anything else as float64 — the reference's
+    np.asarray(coeffs, dtype=np.float64) either way."""
     torch = nat.torch()
-    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float32))
+    c = np.asarray(coeffs)
+    is_f64 = c.dtype != np.float32
+    c = np.ascontiguousarray(c, dtype=np.float64 if is_f64 else np.float32)
     shape = c.shape
-    n = shape[-1]
+    n = shape[-1] if c.ndim else 1
+    if n != stats.n_coeffs:
+        raise ParameterError("coefficient count does not match MAD stats")
     cd = torch.from_numpy(c.reshape(-1, n)).cuda()
     med = torch.from_numpy(np.ascontiguousarray(stats.median, np.float64)).cuda()
     mad = torch.from_numpy(np.ascontiguousarray(stats.mad, np.float64)).cuda()
     out = torch.empty(cd.shape, dtype=torch.float64, device="cuda")
-    nat.call("qs_fp_normalize", nat.ptr(cd), cd.shape[0], n, nat.ptr(med), nat.ptr(mad),
-             nat.ptr(out), nat.stream())
+    nat.call("qs_fp_normalize", nat.ptr(cd), int(is_f64), cd.shape[0], n, nat.ptr(med),
+             nat.ptr(mad), nat.ptr(out), nat.stream())
     return out.cpu().numpy().reshape(shape)
 
 

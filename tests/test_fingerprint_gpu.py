@@ -139,6 +139,13 @@ def test_topk_oracle_ties_and_signs(fp):
     scores = fp.normalize(c, stats)
     want = np.where(mad > 0, (c.astype(np.float64) - med) / np.where(mad > 0, mad, 1.0), 0.0)
     np.testing.assert_allclose(scores, want, rtol=1e-15, atol=0)
+    # float64 input stays float64 (the reference's np.asarray(coeffs, float64))
+    c64 = rng.standard_normal((7, n)) * 1e-3 + 1.0 / 3.0
+    want64 = np.where(mad > 0, (c64 - med) / np.where(mad > 0, mad, 1.0), 0.0)
+    assert np.array_equal(fp.normalize(c64, stats), want64)
+    from paper_1803_09835_b200.errors import ParameterError
+    with pytest.raises(ParameterError):
+        fp.normalize(np.zeros((2, n + 1), np.float32), stats)
 
 
 def test_errors(fp):

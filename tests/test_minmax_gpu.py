@@ -140,3 +140,28 @@ def test_host_pipelined_search_layout_matches_device(mh):
     bad[4321, 7] = 4096
     got = ls.signatures_for_search_host(bad, m, chunk_bytes=1000 * bits.shape[1] * 4)
     assert int(got[3].item()) == 1
+
+
+def test_large_d_plan_free_path():
+    """d > 16384 (e.g. freq_bins=64, time_bins=256 -> d = 32768) takes the
+    plan-free kernel (the reference's elementwise min/max loop): bit-identical
+    to the C oracle, directly and through the search layout."""
+    from oracle import minmax as omm
+    from paper_1803_09835_b200 import lsh_search as ls
+    from paper_1803_09835_b200 import minmax_hash as mh
+    rng = np.random.default_rng(12)
+    d, K, n = 32768, 120, 300
+    bits = np.stack([np.sort(rng.choice(d, K, replace=False)) for _ in range(n)]).astype(np.uint32)
+    bits[150] = bits[3]  # a duplicate row -> one pair with sim = t
+    m = mh.gen_hash_mapping(d, 40, 4, 9)
+    sigs = mh.signatures(bits, m)
+    assert np.array_equal(sigs, omm.signatures_c(bits, m.values, 40, 2))
+    cfg = ls.SearchConfig(tables=40, hash_funcs=4, min_matches=2)
+    from paper_1803_09835_b200.fingerprint import FingerprintSet
+    fps = FingerprintSet(d=d, top_k=K, window_len_s=1.0, window_lag_s=1.0,
+                         indices=np.arange(n, dtype=np.uint64), epochs=np.arange(n, dtype=np.float64),
+                         bits=bits)
+    rec, st, _ = ls.search_fingerprints(fps, ls.SearchConfig(tables=40, hash_funcs=4, min_matches=2,
+                                                             near_repeat_exclusion_s=0.0), mapping=m)
+    want, _ = ls.search_signatures(sigs, cfg)
+    assert rec.tobytes() == want.tobytes() and rec.size >= 1
