@@ -445,6 +445,13 @@ int qs_radix_sort_pairs(uint64_t* keys_dev, uint32_t* vals_dev, uint64_t seg_len
 int qs_peak_launch(int kind, uint32_t blocks, uint32_t iters, void* scratch_dev,
                    double* ops_out, void* stream);
 
+/* The north-star design's pair-count table, as a measurement (DESIGN.md
+ * §5.3): n inserts of `distinct` scattered 64-bit pair keys into an
+ * open-addressed table of `slots` (power of two) 12-byte slots (keys u64 then
+ * counts u32, zeroed by the caller); *probes_dev += probes made. */
+int qs_bench_pair_table(uint64_t n, uint64_t distinct, void* table_dev, uint64_t slots,
+                        uint64_t* probes_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -109,6 +109,7 @@ SIGNATURES = {
     "qs_fingerprint_chain_ws_bytes": (_sz, [_u64, _dbl, ctypes.POINTER(FpParamsC), _u64]),
     "qs_fingerprint_chain": (_int, [_p, _int, _u64, _dbl, ctypes.POINTER(FpParamsC), _p, _u64, _p,
                                     _p, _p, ctypes.POINTER(_u64), _p, _sz, _p]),
+    "qs_bench_pair_table": (_int, [_u64, _u64, _p, _u64, _p, _p]),
     "qs_radix_sort_ws_bytes": (_sz, [_u64, _u32]),
     "qs_radix_sort_pairs": (_int, [_p, _p, _u64, _u32, _u32, _p, _p, _p, _sz, _p, _p]),
 }

@@ -16,6 +16,7 @@
 //                   the K-th largest |score| and an index-ordered tie break
 //   k_col_select    per-column radix select for the MAD medians
 #include <math.h>
+#include <stdlib.h>
 
 #include "qs_common.cuh"
 
@@ -396,6 +397,656 @@ __global__ void __launch_bounds__(WIN_THREADS) k_windows(
     }
 }
 
+
+// ------------------------------------------------- one warp per window
+// The BASELINE geometry (32 x 64 images, <= 16 band rows): one WARP per
+// window and no block barriers.  Lane l owns the 8 x 8 pixel tile (8 (l >> 3),
+// 8 (l & 7)): it computes its pixels straight from the time-resampled band
+// (f64, per-warp shared memory), runs Haar levels 1-3 in registers — the
+// 2-D Haar of fingerprint.py:256-300 is, per level, a 2 x 2 butterfly per
+// block (row pass then column pass, the reference's operation order), and
+// only the low-low value feeds the next level — and levels 4-6 with
+// shuffles.  Coefficients are rounded to f32 where the reference rounds
+// (:334), then written out (modes 1, 2) or turned into select keys (mode 3:
+// |v'| bits + 1, 0 when ineligible, the sign of v' in bit 63) in a per-warp
+// array; the K-th largest key is found by a warp radix select (8-bit digits
+// from the first byte where the eligible keys differ; candidate lists by
+// ordered ballot compaction) and the bits are emitted in index order by
+// ballots over the 64 key words.  The resize weights are padded to fixed tap
+// counts per output (zero weights add exact zeros).
+constexpr int WW_WARPS = 8;
+constexpr uint32_t WW_N = 2048, WW_T = 64, WW_NBMAX = 16;
+constexpr uint32_t WW_FT = 2, WW_TT = 3, WW_NWID = 3;  // taps per w_f / w_t output, widths
+constexpr size_t WW_WARP_BYTES = WW_N * 8 + WW_T * WW_NBMAX * 8 + 256 * 4;  // keys | tmp/lists | hist
+constexpr size_t WW_TAB_BYTES = (32 * WW_FT + WW_NWID * WW_T * WW_TT) * 12 + 64;
+constexpr uint64_t WW_SIGN = 1ull << 63;
+
+__global__ void __launch_bounds__(WW_WARPS * 32, 1) k_win_warp(
+    const float* __restrict__ band, WinGeom g, const int64_t* __restrict__ widx,
+    const int32_t* __restrict__ wf_off, const int32_t* __restrict__ wf_idx,
+    const double* __restrict__ wf_val, const int32_t* __restrict__ wt_off,
+    const int32_t* __restrict__ wt_idx, const double* __restrict__ wt_val,
+    const double* __restrict__ med, const double* __restrict__ mad, void* __restrict__ out,
+    uint32_t* __restrict__ flags) {
+    extern __shared__ __align__(16) unsigned char wsm[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    // padded resize tables, once per CTA: tap t of output r at [r * taps + t]
+    double* fv = (double*)wsm;                                    // [32][WW_FT]
+    double* tv = fv + 32 * WW_FT;                                 // [widths][64][WW_TT]
+    int32_t* fi = (int32_t*)(tv + WW_NWID * WW_T * WW_TT);        // [32][WW_FT]
+    int32_t* ti = fi + 32 * WW_FT;                                // [widths][64][WW_TT]
+    const uint32_t nwid = g.wmax - g.wmin + 1;
+    for (uint32_t q = threadIdx.x; q < 32 * WW_FT; q += blockDim.x) {
+        const uint32_t r = q / WW_FT, t = q - r * WW_FT;
+        const int32_t e = wf_off[r] + (int32_t)t;
+        const bool ok = e < wf_off[r + 1];
+        fv[q] = ok ? wf_val[e] : 0.0;
+        fi[q] = ok ? wf_idx[e] : 0;
+    }
+    for (uint32_t q = threadIdx.x; q < nwid * WW_T * WW_TT; q += blockDim.x) {
+        const uint32_t row = q / WW_TT, t = q - row * WW_TT;       // row = width * 64 + Ti
+        const uint32_t wd = row / WW_T, Ti = row - wd * WW_T;
+        const int32_t* to = wt_off + (uint64_t)wd * (WW_T + 1);
+        const int32_t e = to[Ti] + (int32_t)t;
+        const bool ok = e < to[Ti + 1];
+        tv[q] = ok ? wt_val[e] : 0.0;
+        ti[q] = ok ? wt_idx[e] : 0;
+    }
+    __syncthreads();
+    unsigned char* base = wsm + WW_TAB_BYTES + (size_t)warp * WW_WARP_BYTES;
+    uint64_t* keys = (uint64_t*)base;                                 // [2048]
+    double* tmp = (double*)(base + WW_N * 8);                         // [T][nb]
+    uint16_t* la = (uint16_t*)tmp;                                    // lists alias tmp
+    uint16_t* lb = la + WW_N;
+    uint32_t* hist = (uint32_t*)(base + WW_N * 8 + WW_T * WW_NBMAX * 8);
+    const uint32_t nb = g.nb, mode = g.mode;
+    const double s2 = 0.7071067811865475;  // 1.0 / math.sqrt(2.0), as the reference
+    const uint32_t tr = lane >> 3, tc = lane & 7;
+    const uint64_t nwarp = (uint64_t)gridDim.x * WW_WARPS;
+    for (uint64_t wi = (uint64_t)blockIdx.x * WW_WARPS + warp; wi < g.n_win; wi += nwarp) {
+        const uint64_t idx = widx ? (uint64_t)widx[wi] : g.win0 + wi;
+        const uint64_t off = idx * g.lag;
+        const uint64_t c0 = (off + g.hop - 1) / g.hop;
+        const uint64_t c1 = (off + g.win - g.frame) / g.hop + 1;
+        const uint32_t width = (uint32_t)(c1 - c0);
+        // band rows of the window -> per-warp shared memory (aliases the keys,
+        // dead until the Haar), all loads in flight at once
+        const float* bw = band + c0 * nb;
+        float* gs = (float*)keys;
+        __syncwarp();
+        for (uint32_t i = lane; i < width * nb; i += 32) gs[i] = __ldg(bw + i);
+        __syncwarp();
+        // time resample: tmp[Ti][f] = sum_w w_t[Ti, w] band[w][f] (f64, CSR order)
+        const double* tvw = tv + (uint64_t)(width - g.wmin) * WW_T * WW_TT;
+        const int32_t* tiw = ti + (uint64_t)(width - g.wmin) * WW_T * WW_TT;
+#pragma unroll 1
+        for (uint32_t i = lane; i < WW_T * nb; i += 32) {
+            const uint32_t Ti = i / nb, f = i - Ti * nb;
+            double acc = 0.0;
+#pragma unroll
+            for (uint32_t t = 0; t < WW_TT; ++t)
+                acc = fma(tvw[Ti * WW_TT + t], (double)gs[tiw[Ti * WW_TT + t] * nb + f], acc);
+            tmp[i] = acc;
+        }
+        __syncwarp();
+        bool nonfinite = false;
+        uint64_t kmax = 0, kmin = ~0ull;
+        auto emit = [&](uint32_t j, double v) {
+            const float c = (float)v;  // coefficients are stored float32 (fingerprint.py:334)
+            if (mode == 1) {
+                ((float*)out)[wi * WW_N + j] = c;
+            } else if (mode == 2) {
+                ((float*)out)[(uint64_t)j * g.n_win + wi] = c;
+            } else {
+                const double cd = (double)c;
+                if (!isfinite(cd)) nonfinite = true;
+                const double md = __ldg(mad + j);
+                uint64_t k = 0;
+                if (md > 0.0) {
+                    const double sc = __ddiv_rn(__dsub_rn(cd, __ldg(med + j)), md);
+                    const uint64_t m = mag_key(sc) + 1;
+                    kmax = m > kmax ? m : kmax;
+                    kmin = m < kmin ? m : kmin;
+                    k = m | (sc < 0.0 ? WW_SIGN : 0ull);
+                }
+                keys[j] = k;
+            }
+        };
+        // 2 x 2 butterfly of one Haar level block [x00 x01; x10 x11] at block
+        // (bi, bj) of an (h, w) level: emits LH, HL, HH, returns LL; explicit
+        // round-to-nearest ops (no FMA contraction: the reference rounds every
+        // add and multiply, and exact structural zeros depend on it)
+        auto bfly = [&](double x00, double x01, double x10, double x11, uint32_t bi, uint32_t bj,
+                        uint32_t h, uint32_t w) -> double {
+            const double lo0 = __dmul_rn(__dadd_rn(x00, x01), s2), hi0 = __dmul_rn(__dsub_rn(x00, x01), s2);
+            const double lo1 = __dmul_rn(__dadd_rn(x10, x11), s2), hi1 = __dmul_rn(__dsub_rn(x10, x11), s2);
+            emit(bi * WW_T + w / 2 + bj, __dmul_rn(__dadd_rn(hi0, hi1), s2));
+            emit((h / 2 + bi) * WW_T + bj, __dmul_rn(__dsub_rn(lo0, lo1), s2));
+            emit((h / 2 + bi) * WW_T + w / 2 + bj, __dmul_rn(__dsub_rn(hi0, hi1), s2));
+            return __dmul_rn(__dadd_rn(lo0, lo1), s2);
+        };
+        double q00 = 0, q01 = 0, q10 = 0, q11 = 0;  // LL2 of the four 4 x 4 sub-tiles
+#pragma unroll 1
+        for (uint32_t st = 0; st < 4; ++st) {
+            const uint32_t si = st >> 1, sj = st & 1;
+            double px[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const uint32_t r = 8 * tr + 4 * si + a;
+                const double w0 = fv[r * WW_FT], w1 = fv[r * WW_FT + 1];
+                const uint32_t i0 = fi[r * WW_FT], i1 = fi[r * WW_FT + 1];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t c = 8 * tc + 4 * sj + b;
+                    const double acc = fma(w1, tmp[c * nb + i1], fma(w0, tmp[c * nb + i0], 0.0));
+                    px[a][b] = (double)(float)acc;  // images are float32 (fingerprint.py:239-241)
+                }
+            }
+            double l1[2][2];
+#pragma unroll
+            for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+                for (int b2 = 0; b2 < 2; ++b2)
+                    l1[a2][b2] = bfly(px[2 * a2][2 * b2], px[2 * a2][2 * b2 + 1], px[2 * a2 + 1][2 * b2],
+                                      px[2 * a2 + 1][2 * b2 + 1], 4 * tr + 2 * si + a2,
+                                      4 * tc + 2 * sj + b2, 32, 64);
+            const double l2 = bfly(l1[0][0], l1[0][1], l1[1][0], l1[1][1], 2 * tr + si, 2 * tc + sj, 16, 32);
+            q00 = st == 0 ? l2 : q00;
+            q01 = st == 1 ? l2 : q01;
+            q10 = st == 2 ? l2 : q10;
+            q11 = st == 3 ? l2 : q11;
+        }
+        const double ll3 = bfly(q00, q01, q10, q11, tr, tc, 8, 16);
+        // level 4 (4 x 8): 2 x 2 lane blocks, computed by the even (tr, tc) lanes
+        const double n01 = __shfl_down_sync(0xffffffffu, ll3, 1);
+        const double n10 = __shfl_down_sync(0xffffffffu, ll3, 8);
+        const double n11 = __shfl_down_sync(0xffffffffu, ll3, 9);
+        double ll4 = 0.0;
+        if (!(tr & 1) && !(tc & 1)) ll4 = bfly(ll3, n01, n10, n11, tr / 2, tc / 2, 4, 8);
+        // level 5 (2 x 4): LL4 of block (bi4, bj4) lives in lane 16 bi4 + 2 bj4
+        const double m01 = __shfl_down_sync(0xffffffffu, ll4, 2);
+        const double m10 = __shfl_down_sync(0xffffffffu, ll4, 16);
+        const double m11 = __shfl_down_sync(0xffffffffu, ll4, 18);
+        double ll5 = 0.0;
+        if (lane == 0 || lane == 4) ll5 = bfly(ll4, m01, m10, m11, 0, lane / 4, 2, 4);
+        // level 6 (1 x 2, row pass only)
+        const double x1 = __shfl_down_sync(0xffffffffu, ll5, 4);
+        if (lane == 0) {
+            emit(0, __dmul_rn(__dadd_rn(ll5, x1), s2));
+            emit(1, __dmul_rn(__dsub_rn(ll5, x1), s2));
+        }
+        if (mode != 3) continue;
+        if (__any_sync(0xffffffffu, nonfinite)) {
+            if (lane == 0) atomicOr(flags, 1u);
+            continue;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t a2 = __shfl_xor_sync(0xffffffffu, kmax, o);
+            const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmin, o);
+            kmax = a2 > kmax ? a2 : kmax;
+            kmin = b2 < kmin ? b2 : kmin;
+        }
+        __syncwarp();
+        // ---- the K-th largest key by radix select; bytes above the first one
+        // where eligible keys differ are common to all of them
+        int shift = 56;
+        while (shift > 0 && ((kmax ^ kmin) >> shift) == 0) shift -= 8;
+        uint64_t prefix = shift < 56 ? (kmax >> (shift + 8)) << (shift + 8) : 0ull;
+        uint32_t krem = g.top_k, ncur = WW_N, gt = 0;
+        bool full = true;  // candidates: every coefficient, else the list la
+        for (;; shift -= 8) {
+            for (uint32_t i = lane; i < 256; i += 32) hist[i] = 0;
+            __syncwarp();
+            const uint64_t hmask = shift < 56 ? ~0ull << (shift + 8) : 0ull;
+            for (uint32_t j0 = 0; j0 < ncur; j0 += 32) {
+                const uint32_t jj = j0 + lane;
+                uint32_t d = 256;
+                if (jj < ncur) {
+                    const uint64_t k = keys[full ? jj : la[jj]] & ~WW_SIGN;
+                    if (k && (k & hmask) == prefix) d = (uint32_t)(k >> shift) & 0xFFu;
+                }
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                if (d < 256 && (peers & lt) == 0) atomicAdd(&hist[d], __popc(peers));
+            }
+            __syncwarp();
+            // the digit holding the krem-th largest: lane l owns bins [8l, 8l + 8)
+            uint32_t c[8], sum = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                c[e] = hist[8 * lane + e];
+                sum += c[e];
+            }
+            uint32_t x = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
+                if (lane + o < 32) x += y;
+            }
+            const uint32_t above = x - sum;
+            uint32_t dsel = 0, knew = 0, cgt = 0;
+            const bool mine = above < krem && krem <= x;
+            if (mine) {
+                uint32_t cum = above;
+                dsel = 8 * lane;
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    if (cum + c[e] >= krem) {
+                        dsel = 8 * lane + e;
+                        break;
+                    }
+                    cum += c[e];
+                }
+                knew = krem - cum;
+                cgt = cum;  // candidates in digits above the selected one
+            }
+            const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+            dsel = __shfl_sync(0xffffffffu, dsel, owner);
+            krem = __shfl_sync(0xffffffffu, knew, owner);
+            gt += __shfl_sync(0xffffffffu, cgt, owner);
+            prefix |= (uint64_t)dsel << shift;
+            if (shift == 0) break;
+            // keep the candidates matching the selected digit (ordered compaction)
+            const uint64_t kmask = ~0ull << shift;
+            uint32_t nn = 0;
+            __syncwarp();
+            for (uint32_t j0 = 0; j0 < ncur; j0 += 32) {
+                const uint32_t jj = j0 + lane;
+                bool keep = false;
+                uint32_t j = 0;
+                if (jj < ncur) {
+                    j = full ? jj : la[jj];
+                    const uint64_t k = keys[j] & ~WW_SIGN;
+                    keep = k && (k & kmask) == prefix;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) lb[nn + __popc(bal & lt)] = (uint16_t)j;
+                nn += __popc(bal);
+            }
+            __syncwarp();
+            uint16_t* t2 = la; la = lb; lb = t2;
+            ncur = nn;
+            full = false;
+        }
+        const uint64_t thr = prefix;  // the key of the K-th largest
+        // emission in index order: word i of the key bitmap = keys 32 i .. 32 i + 31
+        const uint32_t need = g.top_k - gt;
+        uint32_t eqseen = 0, pos = 0;
+        uint32_t* ob = (uint32_t*)out + wi * g.top_k;
+        for (uint32_t i = 0; i < WW_N / 32; ++i) {
+            const uint32_t j = 32 * i + lane;
+            const uint64_t kw = keys[j], k = kw & ~WW_SIGN;
+            const uint32_t beq = __ballot_sync(0xffffffffu, k == thr);
+            const bool take = k > thr || (k == thr && eqseen + __popc(beq & lt) < need);
+            const uint32_t bt = __ballot_sync(0xffffffffu, take);
+            if (take) ob[pos + __popc(bt & lt)] = 2 * j + (uint32_t)(kw >> 63);
+            pos += __popc(bt);
+            eqseen += __popc(beq);
+        }
+        la = (uint16_t*)tmp;  // list parity back to the fixed regions
+        lb = la + WW_N;
+    }
+}
+
+// ------------------------------------------- one CTA per window, 32 x 64
+// The same arithmetic as k_windows for the BASELINE geometry (32 x 64 images,
+// <= 16 band rows) with far fewer instructions and barriers: fixed-tap
+// resample weights (zero taps add exact zeros), the 2-D Haar as per-level
+// 2 x 2 butterflies (row pass then column pass per block, the reference's
+// operation order — thread per block, the low-low value handed to the next
+// level; levels 4-6 in one warp by shuffles), coefficients rounded to f32 and
+// turned into select keys once (|v'| bits + 1, 0 when ineligible, the sign in
+// bit 63), a radix select over the stored keys with shrinking candidate
+// lists, and the bits emitted in index order by per-warp ballots.
+constexpr int WC_T = 256, WC_W = WC_T / 32;
+constexpr uint32_t WC_N = 2048, WC_T64 = 64;
+constexpr uint32_t WC_FT = 2, WC_TT = 3, WC_NWID = 3;
+constexpr uint64_t WC_SIGN = 1ull << 63;
+// shared layout (bytes): keys u64[2048] (band rows alias it before the Haar) |
+// tmp f64[64 * 16] (candidate lists alias it after level 1) | ll1 f64[512] |
+// ll2 f64[128] | level-3+ coefficients f32[128] | hist u32[256] | tables
+constexpr size_t WC_OFF_TMP = WC_N * 8, WC_OFF_LL1 = WC_OFF_TMP + 64 * 16 * 8;
+constexpr size_t WC_OFF_LL2 = WC_OFF_LL1 + 512 * 8, WC_OFF_LL3 = WC_OFF_LL2 + 128 * 8;
+constexpr size_t WC_OFF_HIST = WC_OFF_LL3 + 64 * 8, WC_OFF_TAB = WC_OFF_HIST + 256 * 4;
+constexpr size_t WC_SMEM = WC_OFF_TAB + (32 * WC_FT + WC_NWID * 64 * WC_TT) * 12 + 64;
+
+__global__ void __launch_bounds__(WC_T, 4) k_win_cta(
+    const float* __restrict__ band, WinGeom g, const int64_t* __restrict__ widx,
+    const int32_t* __restrict__ wf_off, const int32_t* __restrict__ wf_idx,
+    const double* __restrict__ wf_val, const int32_t* __restrict__ wt_off,
+    const int32_t* __restrict__ wt_idx, const double* __restrict__ wt_val,
+    const double* __restrict__ med, const double* __restrict__ mad, void* __restrict__ out,
+    uint32_t* __restrict__ flags) {
+    extern __shared__ __align__(16) unsigned char csm[];
+    uint64_t* keys = (uint64_t*)csm;
+    float* gs = (float*)csm;
+    double* tmp = (double*)(csm + WC_OFF_TMP);
+    uint16_t* la = (uint16_t*)tmp;
+    uint16_t* lb = la + WC_N;
+    double* ll1 = (double*)(csm + WC_OFF_LL1);
+    double* ll2 = (double*)(csm + WC_OFF_LL2);
+    double* ll3 = (double*)(csm + WC_OFF_LL3);
+    uint32_t* hist = (uint32_t*)(csm + WC_OFF_HIST);
+    double* fv = (double*)(csm + WC_OFF_TAB);
+    double* tv = fv + 32 * WC_FT;
+    int32_t* fi = (int32_t*)(tv + WC_NWID * 64 * WC_TT);
+    int32_t* ti = fi + 32 * WC_FT;
+    __shared__ uint32_t s_nf, s_wcnt[WC_W], s_wcnt2[WC_W], s_ncur;
+    __shared__ uint32_t s_dsel, s_krem, s_gt;
+    __shared__ uint64_t s_kmax, s_kmin;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    const uint32_t nwid = g.wmax - g.wmin + 1, nb = g.nb, mode = g.mode;
+    for (uint32_t q = threadIdx.x; q < 32 * WC_FT; q += WC_T) {
+        const uint32_t r = q / WC_FT, t = q - r * WC_FT;
+        const int32_t e = wf_off[r] + (int32_t)t;
+        const bool ok = e < wf_off[r + 1];
+        fv[q] = ok ? wf_val[e] : 0.0;
+        fi[q] = ok ? wf_idx[e] : 0;
+    }
+    for (uint32_t q = threadIdx.x; q < nwid * 64 * WC_TT; q += WC_T) {
+        const uint32_t row = q / WC_TT, t = q - row * WC_TT;
+        const uint32_t wd = row / 64, Ti = row - wd * 64;
+        const int32_t* to = wt_off + (uint64_t)wd * 65;
+        const int32_t e = to[Ti] + (int32_t)t;
+        const bool ok = e < to[Ti + 1];
+        tv[q] = ok ? wt_val[e] : 0.0;
+        ti[q] = ok ? wt_idx[e] : 0;
+    }
+    const double s2 = 0.7071067811865475;  // 1.0 / math.sqrt(2.0), as the reference
+    for (uint64_t wi = blockIdx.x; wi < g.n_win; wi += gridDim.x) {
+        const uint64_t idx = widx ? (uint64_t)widx[wi] : g.win0 + wi;
+        const uint64_t off = idx * g.lag;
+        const uint64_t c0 = (off + g.hop - 1) / g.hop;
+        const uint64_t c1 = (off + g.win - g.frame) / g.hop + 1;
+        const uint32_t width = (uint32_t)(c1 - c0);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_nf = 0;
+            s_kmax = 0;
+            s_kmin = ~0ull;
+        }
+        for (uint32_t i = threadIdx.x; i < width * nb; i += WC_T) gs[i] = __ldg(band + c0 * nb + i);
+        __syncthreads();
+        // time resample (f64, CSR order; padded taps add exact zeros)
+        const double* tvw = tv + (uint64_t)(width - g.wmin) * 64 * WC_TT;
+        const int32_t* tiw = ti + (uint64_t)(width - g.wmin) * 64 * WC_TT;
+        for (uint32_t i = threadIdx.x; i < 64 * nb; i += WC_T) {
+            const uint32_t Ti = i / nb, f = i - Ti * nb;
+            double acc = 0.0;
+#pragma unroll
+            for (uint32_t t = 0; t < WC_TT; ++t)
+                acc = fma(tvw[Ti * WC_TT + t], (double)gs[tiw[Ti * WC_TT + t] * nb + f], acc);
+            tmp[i] = acc;
+        }
+        __syncthreads();
+        bool nonfinite = false;
+        uint64_t kmax = 0, kmin = ~0ull;
+        auto emit = [&](uint32_t j, double v) {
+            const float c = (float)v;  // coefficients are stored float32 (fingerprint.py:334)
+            if (mode == 1) {
+                ((float*)out)[wi * WC_N + j] = c;
+            } else if (mode == 2) {
+                ((float*)out)[(uint64_t)j * g.n_win + wi] = c;
+            } else {
+                const double cd = (double)c;
+                if (!isfinite(cd)) nonfinite = true;
+                const double md = __ldg(mad + j);
+                uint64_t k = 0;
+                if (md > 0.0) {
+                    const double sc = __ddiv_rn(__dsub_rn(cd, __ldg(med + j)), md);
+                    const uint64_t m = mag_key(sc) + 1;
+                    kmax = m > kmax ? m : kmax;
+                    kmin = m < kmin ? m : kmin;
+                    k = m | (sc < 0.0 ? WC_SIGN : 0ull);
+                }
+                keys[j] = k;
+            }
+        };
+        auto bfly = [&](double x00, double x01, double x10, double x11, uint32_t bi, uint32_t bj,
+                        uint32_t h, uint32_t w) -> double {
+            const double lo0 = __dmul_rn(__dadd_rn(x00, x01), s2), hi0 = __dmul_rn(__dsub_rn(x00, x01), s2);
+            const double lo1 = __dmul_rn(__dadd_rn(x10, x11), s2), hi1 = __dmul_rn(__dsub_rn(x10, x11), s2);
+            emit(bi * 64 + w / 2 + bj, __dmul_rn(__dadd_rn(hi0, hi1), s2));
+            emit((h / 2 + bi) * 64 + bj, __dmul_rn(__dsub_rn(lo0, lo1), s2));
+            emit((h / 2 + bi) * 64 + w / 2 + bj, __dmul_rn(__dsub_rn(hi0, hi1), s2));
+            return __dmul_rn(__dadd_rn(lo0, lo1), s2);
+        };
+        // level 1 (32 x 64): block (bi, bj) = pixels rows 2bi, 2bi+1, cols 2bj, 2bj+1
+        for (uint32_t bk = threadIdx.x; bk < 512; bk += WC_T) {
+            const uint32_t bi = bk >> 5, bj = bk & 31;
+            double x[2][2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const uint32_t r = 2 * bi + a;
+                const double w0 = fv[r * WC_FT], w1 = fv[r * WC_FT + 1];
+                const uint32_t i0 = fi[r * WC_FT], i1 = fi[r * WC_FT + 1];
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t c = 2 * bj + b;
+                    const double acc = fma(w1, tmp[c * nb + i1], fma(w0, tmp[c * nb + i0], 0.0));
+                    x[a][b] = (double)(float)acc;  // images are float32 (fingerprint.py:239-241)
+                }
+            }
+            ll1[bk] = bfly(x[0][0], x[0][1], x[1][0], x[1][1], bi, bj, 32, 64);
+        }
+        __syncthreads();
+        if (threadIdx.x < 128) {  // level 2 (16 x 32)
+            const uint32_t bi = threadIdx.x >> 4, bj = threadIdx.x & 15;
+            ll2[threadIdx.x] = bfly(ll1[(2 * bi) * 32 + 2 * bj], ll1[(2 * bi) * 32 + 2 * bj + 1],
+                                    ll1[(2 * bi + 1) * 32 + 2 * bj], ll1[(2 * bi + 1) * 32 + 2 * bj + 1],
+                                    bi, bj, 16, 32);
+        }
+        __syncthreads();
+        // levels 3-6 in one warp; their 128 coefficients (rows < 8, cols < 16)
+        // go to a small f32 array (ll3 region) and are scored by 128 threads
+        // after the barrier (the divisions stay off warp 0's critical path)
+        float* c3 = (float*)ll3;  // [8][16]
+        if (warp == 0) {
+            auto emit3 = [&](uint32_t j, double v) {
+                const float c = (float)v;
+                if (mode == 1) ((float*)out)[wi * WC_N + j] = c;
+                else if (mode == 2) ((float*)out)[(uint64_t)j * g.n_win + wi] = c;
+                else c3[(j >> 6) * 16 + (j & 63)] = c;
+            };
+            auto bfly3 = [&](double x00, double x01, double x10, double x11, uint32_t bi, uint32_t bj,
+                             uint32_t h, uint32_t w) -> double {
+                const double lo0 = __dmul_rn(__dadd_rn(x00, x01), s2), hi0 = __dmul_rn(__dsub_rn(x00, x01), s2);
+                const double lo1 = __dmul_rn(__dadd_rn(x10, x11), s2), hi1 = __dmul_rn(__dsub_rn(x10, x11), s2);
+                emit3(bi * 64 + w / 2 + bj, __dmul_rn(__dadd_rn(hi0, hi1), s2));
+                emit3((h / 2 + bi) * 64 + bj, __dmul_rn(__dsub_rn(lo0, lo1), s2));
+                emit3((h / 2 + bi) * 64 + w / 2 + bj, __dmul_rn(__dsub_rn(hi0, hi1), s2));
+                return __dmul_rn(__dadd_rn(lo0, lo1), s2);
+            };
+            const uint32_t tr = lane >> 3, tc = lane & 7;  // level-3 block (tr, tc) of 4 x 8
+            const double l3 = bfly3(ll2[(2 * tr) * 16 + 2 * tc], ll2[(2 * tr) * 16 + 2 * tc + 1],
+                                    ll2[(2 * tr + 1) * 16 + 2 * tc], ll2[(2 * tr + 1) * 16 + 2 * tc + 1],
+                                    tr, tc, 8, 16);
+            const double n01 = __shfl_down_sync(0xffffffffu, l3, 1);
+            const double n10 = __shfl_down_sync(0xffffffffu, l3, 8);
+            const double n11 = __shfl_down_sync(0xffffffffu, l3, 9);
+            double l4 = 0.0;
+            if (!(tr & 1) && !(tc & 1)) l4 = bfly3(l3, n01, n10, n11, tr / 2, tc / 2, 4, 8);
+            const double m01 = __shfl_down_sync(0xffffffffu, l4, 2);
+            const double m10 = __shfl_down_sync(0xffffffffu, l4, 16);
+            const double m11 = __shfl_down_sync(0xffffffffu, l4, 18);
+            double l5 = 0.0;
+            if (lane == 0 || lane == 4) l5 = bfly3(l4, m01, m10, m11, 0, lane / 4, 2, 4);
+            const double x1 = __shfl_down_sync(0xffffffffu, l5, 4);
+            if (lane == 0) {
+                emit3(0, __dmul_rn(__dadd_rn(l5, x1), s2));
+                emit3(1, __dmul_rn(__dsub_rn(l5, x1), s2));
+            }
+        }
+        if (mode != 3) continue;
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            const uint32_t j = (threadIdx.x >> 4) * 64 + (threadIdx.x & 15);
+            emit(j, (double)c3[threadIdx.x]);
+        }
+        // CTA-wide non-finite flag, key range
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t a2 = __shfl_xor_sync(0xffffffffu, kmax, o);
+            const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmin, o);
+            kmax = a2 > kmax ? a2 : kmax;
+            kmin = b2 < kmin ? b2 : kmin;
+        }
+        if (__any_sync(0xffffffffu, nonfinite) && lane == 0) s_nf = 1;
+        if (lane == 0) {
+            atomicMax((unsigned long long*)&s_kmax, (unsigned long long)kmax);
+            atomicMin((unsigned long long*)&s_kmin, (unsigned long long)kmin);
+        }
+        __syncthreads();
+        if (s_nf) {
+            if (threadIdx.x == 0) atomicOr(flags, 1u);
+            continue;
+        }
+        kmax = s_kmax;
+        kmin = s_kmin;
+        // 8-bit digits starting at the highest bit where the eligible keys
+        // differ (bits above it are common to all of them); the last digit may
+        // overlap decided bits (constant over the candidates)
+        const uint64_t dk = kmax ^ kmin;
+        int shift = dk ? max(0, 63 - __clzll((long long)dk) - 7) : 0;
+        uint64_t decided = shift + 8 < 64 ? ~0ull << (shift + 8) : 0ull;
+        uint64_t prefix = kmax & decided;
+        uint32_t krem = g.top_k, ncur = WC_N, gt = 0;
+        bool full = true;
+        uint16_t* cur = la;
+        uint16_t* nxt = lb;
+        bool done = false;
+        for (;;) {
+            for (uint32_t i = threadIdx.x; i < 256; i += WC_T) hist[i] = 0;
+            __syncthreads();
+            const uint64_t hmask = decided;
+            for (uint32_t jj = threadIdx.x; jj < ncur; jj += WC_T) {
+                const uint64_t k = keys[full ? jj : cur[jj]] & ~WC_SIGN;
+                if (k && (k & hmask) == prefix) atomicAdd(&hist[(uint32_t)(k >> shift) & 0xFFu], 1u);
+            }
+            if (threadIdx.x == 0) s_ncur = 0;
+            __syncthreads();
+            // every warp finds the digit holding the krem-th largest (no extra barrier)
+            {
+                uint32_t c[8], sum = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    c[e] = hist[8 * lane + e];
+                    sum += c[e];
+                }
+                uint32_t x = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
+                    if (lane + o < 32) x += y;
+                }
+                const uint32_t above = x - sum;
+                const bool mine = above < krem && krem <= x;
+                uint32_t cum = above, dsel = 8 * lane;
+                if (mine) {
+#pragma unroll
+                    for (int e = 7; e >= 0; --e) {
+                        if (cum + c[e] >= krem) {
+                            dsel = 8 * lane + e;
+                            break;
+                        }
+                        cum += c[e];
+                    }
+                }
+                const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+                dsel = __shfl_sync(0xffffffffu, dsel, owner);
+                cum = __shfl_sync(0xffffffffu, cum, owner);
+                krem -= cum;
+                gt += cum;
+                prefix = (prefix & ~(0xFFull << shift)) | ((uint64_t)dsel << shift);
+                decided |= 0xFFull << shift;
+            }
+            if (shift == 0) break;
+            // keep the matching candidates (order is irrelevant for the select)
+            const uint64_t kmask = decided;
+            for (uint32_t j0 = 0; j0 < ncur; j0 += WC_T) {
+                const uint32_t jj = j0 + threadIdx.x;
+                bool keep = false;
+                uint32_t j = 0;
+                if (jj < ncur) {
+                    j = full ? jj : cur[jj];
+                    const uint64_t k = keys[j] & ~WC_SIGN;
+                    keep = k && (k & kmask) == prefix;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                uint32_t wb = 0;
+                if (lane == 0 && bal) wb = atomicAdd(&s_ncur, __popc(bal));
+                wb = __shfl_sync(0xffffffffu, wb, 0);
+                if (keep) nxt[wb + __popc(bal & lt)] = (uint16_t)j;
+            }
+            __syncthreads();
+            ncur = s_ncur;
+            uint16_t* t2 = cur; cur = nxt; nxt = t2;
+            full = false;
+            shift = shift >= 8 ? shift - 8 : 0;
+            if (ncur <= 32) {  // the rest by ranks inside one warp
+                if (warp == 0) {
+                    const uint64_t k = lane < ncur ? keys[cur[lane]] & ~WC_SIGN : 0ull;
+                    uint32_t greater = 0, geq = 0;
+                    for (uint32_t m = 0; m < ncur; ++m) {
+                        const uint64_t km = __shfl_sync(0xffffffffu, k, m);
+                        greater += km > k;
+                        geq += km >= k;
+                    }
+                    const bool hit = lane < ncur && greater < krem && krem <= geq;
+                    const uint32_t own = __ffs(__ballot_sync(0xffffffffu, hit)) - 1;
+                    if (lane == own) {
+                        s_kmax = k;        // the threshold key
+                        s_dsel = greater;  // candidates above it
+                    }
+                }
+                __syncthreads();
+                prefix = s_kmax;
+                gt += s_dsel;
+                done = true;
+                break;
+            }
+        }
+        (void)done;
+        const uint64_t thr = prefix;
+        const uint32_t need = g.top_k - gt;
+        // emission in index order: warp w owns key words 8w .. 8w + 7 (keys
+        // 256 w .. 256 w + 255); per-warp counts of ties and takes, then prefixes
+        uint32_t beqs[8], ntie = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t k = keys[256 * warp + 32 * q + lane] & ~WC_SIGN;
+            beqs[q] = __ballot_sync(0xffffffffu, k == thr);
+            ntie += __popc(beqs[q]);
+        }
+        if (lane == 0) s_wcnt[warp] = ntie;
+        __syncthreads();
+        uint32_t eqseen = 0;
+        for (uint32_t w = 0; w < warp; ++w) eqseen += s_wcnt[w];
+        uint32_t takes[8], ntake = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint64_t k = keys[256 * warp + 32 * q + lane] & ~WC_SIGN;
+            const bool take = k > thr || (k == thr && eqseen + __popc(beqs[q] & lt) < need);
+            takes[q] = __ballot_sync(0xffffffffu, take);
+            ntake += __popc(takes[q]);
+            eqseen += __popc(beqs[q]);
+        }
+        if (lane == 0) s_wcnt2[warp] = ntake;
+        __syncthreads();
+        uint32_t pos = 0;
+        for (uint32_t w = 0; w < warp; ++w) pos += s_wcnt2[w];
+        uint32_t* ob = (uint32_t*)out + wi * g.top_k;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t j = 256 * warp + 32 * q + lane;
+            if ((takes[q] >> lane) & 1u)
+                ob[pos + __popc(takes[q] & lt)] = 2 * j + (uint32_t)(keys[j] >> 63);
+            pos += __popc(takes[q]);
+        }
+    }
+}
+
 // ------------------------------------------------------------ MAD select
 // Order statistic k of each column (n_cols columns of S values).  mode 0:
 // values x (f32 widened to f64); mode 1: |x - center[col]| (f64).  Radix
@@ -450,6 +1101,148 @@ __global__ void __launch_bounds__(512) k_col_select(const float* __restrict__ co
         __syncthreads();
     }
     if (threadIdx.x == 0) out[col] = key_val(s_prefix);
+}
+
+// Median / MAD of one column per CTA in few passes over the column: the
+// order statistic k by 12-bit digits over the order-preserving 64-bit keys
+// of the f64 values, starting at the highest bit where the column's min and
+// max keys differ; once the bin holding rank k has <= MS_CAP members they
+// are compacted into shared memory and ranked there (bitonic sort), so a
+// column is read ~3 times instead of 8 per order statistic.  For an even
+// count the upper middle value comes from one more pass (count <= v, min
+// above v), then (a + b) / 2 in f64 as np.median.  mode 1: |x - center|.
+constexpr int MS_T = 512;
+constexpr uint32_t MS_CAP = 1024, MS_BINS = 4096;
+
+__device__ __forceinline__ double ms_val(const float* c, uint64_t i, int mode, double ctr) {
+    return mode ? fabs((double)c[i] - ctr) : (double)c[i];
+}
+
+__device__ uint64_t ms_reduce_u64(uint64_t v, bool is_max, uint64_t* red) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? (w > v ? w : v) : (w < v ? w : v);
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    v = red[0];
+    for (int w = 1; w < MS_T / 32; ++w) v = is_max ? (red[w] > v ? red[w] : v) : (red[w] < v ? red[w] : v);
+    return v;
+}
+
+__global__ void __launch_bounds__(MS_T) k_col_median(const float* __restrict__ cols, uint64_t S,
+                                                     int mode, const double* __restrict__ center,
+                                                     double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char msm[];
+    uint32_t* hist = (uint32_t*)msm;                               // [MS_BINS]
+    uint64_t* lst = (uint64_t*)(msm + MS_BINS * 4);                 // [MS_CAP]
+    __shared__ uint64_t red[MS_T / 32];
+    __shared__ uint32_t s_cnt, s_bin, s_below;
+    const uint32_t col = blockIdx.x;
+    const float* c = cols + (uint64_t)col * S;
+    const double ctr = mode ? center[col] : 0.0;
+    uint64_t kmin = ~0ull, kmax = 0;
+    for (uint64_t i = threadIdx.x; i < S; i += MS_T) {
+        const uint64_t k = ord_key(ms_val(c, i, mode, ctr));
+        kmin = k < kmin ? k : kmin;
+        kmax = k > kmax ? k : kmax;
+    }
+    kmin = ms_reduce_u64(kmin, false, red);
+    kmax = ms_reduce_u64(kmax, true, red);
+    uint64_t rank = (S - 1) / 2;  // lower middle (the middle for odd S)
+    const uint64_t dk = kmin ^ kmax;
+    int shift = dk ? max(0, 63 - __clzll((long long)dk) - 11) : 0;
+    uint64_t decided = shift + 12 < 64 ? ~0ull << (shift + 12) : 0ull;
+    uint64_t prefix = kmin & decided;
+    uint64_t v1key = 0;
+    while (true) {
+        for (uint32_t b = threadIdx.x; b < MS_BINS; b += MS_T) hist[b] = 0;
+        __syncthreads();
+        for (uint64_t i = threadIdx.x; i < S; i += MS_T) {
+            const uint64_t k = ord_key(ms_val(c, i, mode, ctr));
+            if ((k & decided) == prefix) atomicAdd(&hist[(k >> shift) & 0xFFF], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {  // the bin holding `rank` (ascending)
+            uint64_t cum = 0;
+            uint32_t b = 0;
+            for (; b < MS_BINS; ++b) {
+                if (cum + hist[b] > rank) break;
+                cum += hist[b];
+            }
+            s_bin = b;
+            s_below = (uint32_t)cum;
+            s_cnt = hist[b];
+        }
+        __syncthreads();
+        const uint32_t bin = s_bin, cnt = s_cnt;
+        rank -= s_below;
+        prefix = (prefix & ~(0xFFFull << shift)) | ((uint64_t)bin << shift);
+        decided |= 0xFFFull << shift;
+        if (cnt <= MS_CAP || shift == 0) {
+            if (cnt > MS_CAP) {  // every remaining bit decided: the key itself
+                v1key = prefix;
+                break;
+            }
+            // compact the bin into shared memory and rank it there
+            if (threadIdx.x == 0) s_cnt = 0;
+            __syncthreads();
+            for (uint64_t i = threadIdx.x; i < S; i += MS_T) {
+                const uint64_t k = ord_key(ms_val(c, i, mode, ctr));
+                if ((k & decided) == prefix) lst[atomicAdd(&s_cnt, 1u)] = k;
+            }
+            __syncthreads();
+            const uint32_t L = s_cnt;
+            uint32_t P = 1;
+            while (P < L) P <<= 1;
+            for (uint32_t i = L + threadIdx.x; i < P; i += MS_T) lst[i] = ~0ull;
+            __syncthreads();
+            for (uint32_t kk = 2; kk <= P; kk <<= 1)
+                for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+                    for (uint32_t i = threadIdx.x; i < P; i += MS_T) {
+                        const uint32_t l = i ^ j;
+                        if (l > i) {
+                            const uint64_t a = lst[i], b2 = lst[l];
+                            const bool up = (i & kk) == 0;
+                            if ((a > b2) == up) {
+                                lst[i] = b2;
+                                lst[l] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            v1key = lst[rank];
+            break;
+        }
+        shift = shift >= 12 ? shift - 12 : 0;
+    }
+    double v = key_val(v1key);
+    if (!(S & 1)) {
+        // upper middle: v again when it repeats past the lower rank, else the
+        // smallest value above it
+        const uint64_t lower = (S - 1) / 2;
+        uint64_t le = 0, above = ~0ull;
+        for (uint64_t i = threadIdx.x; i < S; i += MS_T) {
+            const uint64_t k = ord_key(ms_val(c, i, mode, ctr));
+            le += k <= v1key;
+            if (k > v1key && k < above) above = k;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) le += __shfl_xor_sync(0xffffffffu, le, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = le;
+        __syncthreads();
+        uint64_t tle = 0;
+        for (int w = 0; w < MS_T / 32; ++w) tle += red[w];
+        above = ms_reduce_u64(above, false, red);
+        const double v2 = tle > lower + 1 ? v : key_val(above);
+        v = (v + v2) / 2.0;  // np.median of an even count
+    }
+    if (threadIdx.x == 0) out[col] = v;
 }
 
 __global__ void k_mid_mean(const double* __restrict__ a, const double* __restrict__ b, uint32_t n,
@@ -629,6 +1422,13 @@ int qs_fp_band_stft(const void* x_dev, int x_is_f32, uint64_t n_samples, uint32_
     return QS_OK;
 }
 
+static int num_sms_fp() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
 int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int64_t* widx_dev,
                   uint64_t win0, uint64_t n_win, uint64_t lag, uint64_t win, uint32_t frame,
                   uint32_t hop, const int32_t* wf_off, const int32_t* wf_idx, const double* wf_val,
@@ -641,11 +1441,47 @@ int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int
     QS_ARG(mode != 3 || (top_k >= 1 && top_k <= F * T), "bad top_k");
     if (n_win == 0) return QS_OK;
     (void)n_cols;
+    WinGeom g{n_cols, lag, win, win0, n_win, frame, hop, nb, F, T, wmin, wmax, n_levels, top_k,
+              (uint32_t)mode};
+    // the BASELINE geometry (32 x 64 images, <= 16 band rows): one warp per window
+    // kernel choice for the BASELINE geometry: QS_WIN_KERNEL = cta32 (default),
+    // warp, generic (k_windows) — A/B measurements
+    static const char* wk = getenv("QS_WIN_KERNEL");
+    static const int kind = !wk ? 0 : (wk[0] == 'w' ? 1 : (wk[0] == 'g' ? 2 : 0));
+    const bool cta_only = kind != 1;
+    // padded resize tables: <= WW_FT taps per w_f row (nb <= 16 upsampled to 32
+    // rows), <= WW_TT per w_t row (width <= 128 resampled to 64), <= WW_NWID widths
+    const bool tabs_fit = nb <= 16 && wmax <= 128 && wmax - wmin + 1 <= WW_NWID;
+    if (!cta_only && mode >= 1 && F == 32 && T == WW_T && nb <= WW_NBMAX && n_levels == 6 &&
+        tabs_fit && (size_t)wmax * nb * 4 <= WW_N * 8) {
+        const size_t wsmem = WW_TAB_BYTES + WW_WARP_BYTES * WW_WARPS;
+        QS_CUDA(cudaFuncSetAttribute(k_win_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)wsmem), "attr");
+        const uint64_t want = (n_win + WW_WARPS - 1) / WW_WARPS;
+        const unsigned grid = (unsigned)(want < (uint64_t)num_sms_fp() ? want : (uint64_t)num_sms_fp());
+        k_win_warp<<<grid, WW_WARPS * 32, wsmem, (cudaStream_t)stream>>>(
+            band_dev, g, widx_dev, wf_off, wf_idx, wf_val, wt_off, wt_idx, wt_val, med_dev, mad_dev,
+            out_dev, flags_dev);
+        QS_CHECK_LAUNCH("k_win_warp");
+        return QS_OK;
+    }
+    if (kind == 0 && mode >= 1 && F == 32 && T == WC_T64 && nb <= 16 && n_levels == 6 && wmax <= 128 &&
+        wmax - wmin + 1 <= WC_NWID && (size_t)wmax * nb * 4 <= WC_N * 8) {
+        QS_CUDA(cudaFuncSetAttribute(k_win_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)WC_SMEM), "attr");
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_win_cta, WC_T, WC_SMEM);
+        const uint64_t cap = (uint64_t)num_sms_fp() * (per_sm < 1 ? 1 : per_sm) * 4;
+        const unsigned grid = (unsigned)(n_win < cap ? n_win : cap);
+        k_win_cta<<<grid, WC_T, WC_SMEM, (cudaStream_t)stream>>>(
+            band_dev, g, widx_dev, wf_off, wf_idx, wf_val, wt_off, wt_idx, wt_val, med_dev, mad_dev,
+            out_dev, flags_dev);
+        QS_CHECK_LAUNCH("k_win_cta");
+        return QS_OK;
+    }
     const size_t smem = win_smem(F, T, wmax, nb).bytes;
     QS_ARG(smem <= 200 * 1024, "spectral image too large for the window kernel");
     QS_CUDA(cudaFuncSetAttribute(k_windows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-    WinGeom g{n_cols, lag, win, win0, n_win, frame, hop, nb, F, T, wmin, wmax, n_levels, top_k,
-              (uint32_t)mode};
     const unsigned grid = (unsigned)(n_win < 148 * 32 ? n_win : 148 * 32);
     k_windows<<<grid, WIN_THREADS, smem, (cudaStream_t)stream>>>(
         band_dev, g, widx_dev, wf_off, wf_idx, wf_val, wt_off, wt_idx, wt_val, sched_dev, med_dev,
@@ -660,6 +1496,17 @@ int qs_fp_mad(const float* cols_dev, uint32_t n_coeffs, uint64_t S, double* med_
     cudaStream_t st = (cudaStream_t)stream;
     double* a = ws_dev;
     double* b = ws_dev + n_coeffs;
+    // QS_MAD_SELECT=radix: the round-1 8-pass radix select per order statistic
+    static const bool radix = getenv("QS_MAD_SELECT") && getenv("QS_MAD_SELECT")[0] == 'r';
+    if (!radix) {
+        const size_t sm = (size_t)MS_BINS * 4 + (size_t)MS_CAP * 8;
+        QS_CUDA(cudaFuncSetAttribute(k_col_median, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                "attr");
+        k_col_median<<<n_coeffs, MS_T, sm, st>>>(cols_dev, S, 0, nullptr, med_dev);
+        k_col_median<<<n_coeffs, MS_T, sm, st>>>(cols_dev, S, 1, med_dev, mad_dev);
+        QS_CHECK_LAUNCH("qs_fp_mad");
+        return QS_OK;
+    }
     for (int pass = 0; pass < 2; ++pass) {
         double* dst = pass == 0 ? med_dev : mad_dev;
         if (S & 1) {

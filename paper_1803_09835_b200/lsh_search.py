@@ -190,9 +190,17 @@ class DeviceSearch:
         self._mark("buckets")
         self.sids = torch.empty((t, n), dtype=torch.int32, device=self.dev)
         flags = torch.empty((t, n), dtype=torch.uint8, device=self.dev)
-        ws = self._empty(lib.qs_lsh_bucket_flags_ws_bytes(n, t))
-        nat.call("qs_lsh_build_bucket_flags", nat.ptr(self.keys), n, t, nat.ptr(self.sids),
-                 nat.ptr(flags), nat.ptr(ws), ws.numel(), nat.stream())
+        # tables are independent: big searches (cfg3: N = 3.15e7) build them in
+        # chunks so the sort workspace (~20 B per member and table) stays bounded
+        budget = float(os.environ.get("QS_BUCKET_WS_GB", "24")) * 2**30
+        per_table = lib.qs_lsh_bucket_flags_ws_bytes(n, 1)
+        tc = max(1, min(t, int(budget // max(1, per_table))))
+        ws = self._empty(lib.qs_lsh_bucket_flags_ws_bytes(n, tc))
+        for t0 in range(0, t, tc):
+            t1 = min(t, t0 + tc)
+            nat.call("qs_lsh_build_bucket_flags", nat.ptr(self.keys[t0:t1]), n, t1 - t0,
+                     nat.ptr(self.sids[t0:t1]), nat.ptr(flags[t0:t1]), nat.ptr(ws), ws.numel(),
+                     nat.stream())
         del ws
         self.launches += 3 * 3 + 5
         self._mark("list")

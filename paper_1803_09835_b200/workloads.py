@@ -223,3 +223,58 @@ def cfg2_trace_torch(n_samples=795_000_000, seed=2, repeats=500, device="cuda", 
             out[int(o):int(o) + wv.size] += float(amp) * wd
             truth.append((ti, int(o), float(amp)))
     return out, truth
+
+
+def cfg3_trace_torch(n_samples=3_150_000_000, seed=3, repeats=2000, periodic=50, period_s=60.0,
+                     periodic_amp=(0.1, 0.3), jitter_s=2.0, device="cuda", chunk=1 << 26):
+    """cfg3 (1 year at 100 Hz) on the GPU: N(0, 1) float32 noise, `repeats`
+    planted copies of the cfg0 chirp templates (amplitude log-uniform
+    0.2..2 x RMS) and `periodic` noise templates repeating every `period_s`.
+
+    The periodic templates are BOUNDED as SURVEY.md §7.2 item 2 requires (an
+    exact repeat every 60 s for a year makes 525,600 near-identical windows per
+    template, whose pairs the reference's occurrence filter must enumerate
+    before it can exclude them): each is weak (amplitude U(0.1, 0.3) x RMS,
+    below the noise) and every repetition is jittered by U(-2, 2) s in 0.1 s
+    steps.  Returns a float32 CUDA tensor and a dict of what was planted."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.empty(n_samples, dtype=torch.float32, device=device)
+    for a in range(0, n_samples, chunk):
+        b = min(n_samples, a + chunk)
+        x[a:b] = torch.randn(b - a, generator=g, device=device, dtype=torch.float32)
+    rng = np.random.default_rng(seed + 1)
+    events = chirp_templates(rng)
+    per = max(1, repeats // len(events))
+    ev_truth = []
+    for ti, wv in enumerate(events):
+        offs = rng.integers(0, n_samples - wv.size, size=per)
+        amps = 10.0 ** rng.uniform(math.log10(0.2), math.log10(2.0), size=per)
+        wd = torch.from_numpy(wv).to(device)
+        for o, amp in zip(offs, amps):
+            x[int(o):int(o) + wv.size] += float(amp) * wd
+            ev_truth.append((ti, int(o), float(amp)))
+    # periodic templates: damped chirps of a second family, one 60 s cell each
+    cell = int(round(period_s * SR_HZ))
+    cells = n_samples // cell
+    view = x[: cells * cell].view(cells, cell)
+    ptemps = chirp_templates(rng, n_templates=periodic, length_s=20.0)
+    L = ptemps[0].size
+    jmax = int(round(jitter_s * 10))
+    span = cell - L - 2 * jmax * 10
+    for p, wv in enumerate(ptemps):
+        amp = float(rng.uniform(*periodic_amp))
+        base = jmax * 10 + (p * span) // max(1, periodic - 1)
+        jit = torch.randint(-jmax, jmax + 1, (cells,), generator=g, device=device) * 10
+        src = torch.zeros((1, cell), dtype=torch.float32, device=device)
+        wd = torch.from_numpy(wv).to(device) * amp
+        for v in range(-jmax, jmax + 1):
+            rows = torch.nonzero(jit == v * 10).view(-1)
+            if rows.numel() == 0:
+                continue
+            s0 = base + v * 10
+            src.zero_()
+            src[0, s0:s0 + L] = wd
+            view.index_add_(0, rows, src.expand(rows.numel(), cell))
+    return x, {"events": ev_truth, "periodic": periodic, "cells": cells}
