@@ -52,6 +52,35 @@ __global__ void __launch_bounds__(PK_THREADS) k_peak_minmax64(uint64_t* __restri
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// The north-star pair-count table (BASELINE.json north_star: "collision
+// counting in an HBM open-addressed hash table"), measured rather than built:
+// every candidate (pair, table) hit inserts its 64-bit pair key into an
+// open-addressed table (linear probing, atomicCAS on the key, atomicAdd on a
+// 32-bit count).  Hit i inserts key fmix64(seed ^ (i mod distinct)), so each
+// of `distinct` pairs is hit n / distinct times in scattered order — the
+// access pattern of counting the hits of a bucket enumeration.
+__global__ void __launch_bounds__(256) k_pair_table(uint64_t n, uint64_t distinct,
+                                                   unsigned long long* __restrict__ keys,
+                                                   uint32_t* __restrict__ cnt, uint64_t mask,
+                                                   unsigned long long* __restrict__ probes) {
+    unsigned long long pr = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = fmix64(0x5851F42D4C957F2Dull ^ (i % distinct)) | 1ull;
+        uint64_t slot = fmix64(k) & mask;
+        while (true) {
+            ++pr;
+            const unsigned long long old = atomicCAS(keys + slot, 0ull, k);
+            if (old == 0ull || old == k) {
+                atomicAdd(cnt + slot, 1u);
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+    }
+    atomicAdd(probes, pr);
+}
+
 }  // namespace qs
 
 using namespace qs;
@@ -78,6 +107,22 @@ int qs_peak_launch(int kind, uint32_t blocks, uint32_t iters, void* scratch_dev,
                                                         0x9E3779B97F4A7C15ull, 0xD1B54A32D192ED03ull);
     QS_CHECK_LAUNCH("k_peak");
     *ops_out = (double)blocks * PK_THREADS * iters * PK_CHAINS;
+    return QS_OK;
+}
+
+// One launch of the pair-count-table insert microbenchmark above: n inserts of
+// `distinct` keys into a table of `slots` (power of two) 12-byte slots at
+// table_dev (keys [slots] u64 then counts [slots] u32, zeroed by the caller);
+// probes_dev (u64, zeroed) receives the probe count.  Time it with events.
+int qs_bench_pair_table(uint64_t n, uint64_t distinct, void* table_dev, uint64_t slots,
+                        uint64_t* probes_dev, void* stream) {
+    QS_ARG(slots >= 2 && (slots & (slots - 1)) == 0, "slots must be a power of two");
+    QS_ARG(distinct >= 1 && distinct < slots, "distinct keys must fit the table");
+    unsigned long long* keys = (unsigned long long*)table_dev;
+    uint32_t* cnt = (uint32_t*)(keys + slots);
+    k_pair_table<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(n, distinct, keys, cnt, slots - 1,
+                                                             (unsigned long long*)probes_dev);
+    QS_CHECK_LAUNCH("k_pair_table");
     return QS_OK;
 }
 

@@ -502,11 +502,33 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
     if params.top_k > n_eligible:
         raise ParameterError(f"top_k={params.top_k} exceeds {n_eligible} coefficients with nonzero MAD")
     bits = torch.empty((total, params.top_k), dtype=torch.int32, device="cuda")
-    ch.windows(3, bits, win0=0, n=total, med=med, mad=mad, top_k=params.top_k)
-    ch.check_finite()
+    if nat.is_device_tensor(ts.samples):
+        ch.windows(3, bits, win0=0, n=total, med=med, mad=mad, top_k=params.top_k)
+        ch.check_finite()
+        out_bits = bits
+    else:
+        # host trace: the main pass runs in window chunks and each chunk's bits
+        # go to pinned host memory on a copy stream while the next chunk
+        # computes (the D2H overlaps the kernel instead of following it)
+        host = torch.empty((total, params.top_k), dtype=torch.int32, pin_memory=True)
+        compute = torch.cuda.current_stream()
+        copy = torch.cuda.Stream()
+        nchunk = 8 if total >= 8 * 4096 else 1
+        step = -(-total // nchunk)
+        for c0 in range(0, total, step):
+            c1 = min(total, c0 + step)
+            ch.windows(3, bits[c0:c1], win0=c0, n=c1 - c0, med=med, mad=mad, top_k=params.top_k)
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                host[c0:c1].copy_(bits[c0:c1], non_blocking=True)
+        bits.record_stream(copy)
+        copy.synchronize()
+        ch.check_finite()
+        out_bits = host.numpy().view(np.uint32)
     indices = np.arange(total, dtype=np.uint64)
     epochs = ts.start_epoch_s + np.arange(total) * params.window_lag_s
-    out_bits = bits if nat.is_device_tensor(ts.samples) else _to_host_pinned(bits).view(np.uint32)
     fps = FingerprintSet(d=params.d, top_k=params.top_k, window_len_s=params.window_len_s,
                          window_lag_s=params.window_lag_s, indices=indices, epochs=epochs,
                          bits=out_bits,
