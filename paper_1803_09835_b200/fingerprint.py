@@ -244,15 +244,6 @@ class _Chain:
         self.freqs = np.fft.rfftfreq(self.frame, 1.0 / sr)
         self.r0, self.r1 = (0, len(self.freqs)) if full_band else _band_rows(self.freqs, params)
         self.nb = self.r1 - self.r0
-        x = ts.samples
-        if nat.is_device_tensor(x):
-            xd = x.contiguous()
-            if xd.dtype not in (torch.float32, torch.float64):
-                xd = xd.to(torch.float64)
-        else:
-            from .lsh_search import _to_device_staged
-            xd = _to_device_staged(np.ascontiguousarray(x, dtype=np.float64))
-        self.x = xd
         taper = np.hanning(self.frame)
         j = np.arange(self.frame)
         k = np.arange(self.r0, self.r1)[:, None]
@@ -260,9 +251,42 @@ class _Chain:
         tw = np.stack([taper * np.cos(ang), -taper * np.sin(ang)], axis=-1)
         self.tw = torch.from_numpy(np.ascontiguousarray(tw)).cuda()
         self.band = torch.empty((max(self.n_cols, 1), self.nb), dtype=torch.float32, device="cuda")
-        nat.call("qs_fp_band_stft", nat.ptr(self.x), int(self.x.dtype == torch.float32),
-                 ts.n_samples, self.frame, self.hop, self.n_cols, self.nb, nat.ptr(self.tw),
-                 nat.ptr(self.band), nat.stream())
+        x = ts.samples
+        n_samples = ts.n_samples
+        frame, hop, nb = self.frame, self.hop, self.nb
+
+        def stft(xd, c_lo, c_hi):
+            # columns [c_lo, c_hi) only read samples [c_lo hop, (c_hi - 1) hop + frame)
+            if c_hi <= c_lo:
+                return
+            es = xd.element_size()
+            nat.call("qs_fp_band_stft", nat.ctypes.c_void_p(xd.data_ptr() + c_lo * hop * es),
+                     int(xd.dtype == torch.float32), n_samples - c_lo * hop, frame, hop,
+                     c_hi - c_lo, nb, nat.ptr(self.tw),
+                     nat.ctypes.c_void_p(self.band.data_ptr() + c_lo * nb * 4), nat.stream())
+
+        if nat.is_device_tensor(x):
+            xd = x.contiguous()
+            if xd.dtype not in (torch.float32, torch.float64):
+                xd = xd.to(torch.float64)
+            stft(xd, 0, self.n_cols)
+        else:
+            # host trace: the STFT of every column whose samples have landed runs
+            # while the later chunks are still being copied
+            from .lsh_search import _to_device_staged
+            holder, state = [], [0]
+
+            def on_chunk(done):
+                c_hi = min(self.n_cols, (done - frame) // hop + 1) if done >= frame else 0
+                stft(holder[0], state[0], c_hi)
+                state[0] = max(state[0], c_hi)
+
+            arr = np.ascontiguousarray(x, dtype=np.float64)
+            xd = torch.empty(arr.shape, dtype=torch.float64, device="cuda")
+            holder.append(xd)
+            xd = _to_device_staged(arr, on_chunk=on_chunk, out=xd)
+            stft(xd, state[0], self.n_cols)
+        self.x = xd
 
     def prepare_windows(self):
         params, torch = self.params, self.torch

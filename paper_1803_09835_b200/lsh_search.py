@@ -538,14 +538,18 @@ def _copy_pool():
     return _COPY_POOL
 
 
-def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
+def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20, on_chunk=None, out=None):
     """Host -> device copy of a pageable numpy array through two pinned staging
     buffers: the host copy into one buffer is split over a thread pool (numpy
-    releases the GIL) while the DMA of the other runs (~44 GB/s on the B200
-    box against ~14 GB/s single-threaded)."""
+    releases the GIL) while the DMA of the other runs on a copy stream (~44
+    GB/s on the B200 box against ~14 GB/s single-threaded).  `on_chunk(done)`
+    is called after each chunk lands, on the compute stream (work on the
+    first `done` elements overlaps the remaining copies).  `out`: an existing
+    CUDA tensor of the same shape and dtype to fill."""
     torch = nat.torch()
     flat = arr.reshape(-1)
-    out = torch.empty(arr.shape, dtype=torch.from_numpy(flat[:0]).dtype, device="cuda")
+    if out is None:
+        out = torch.empty(arr.shape, dtype=torch.from_numpy(flat[:0]).dtype, device="cuda")
     if flat.size == 0:
         return out
     dst = out.view(-1)
@@ -554,6 +558,9 @@ def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
     done = [None, None]
     pool = _copy_pool()
     nthr = pool._max_workers
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    copy.wait_stream(compute)  # dst's allocation is ordered on the compute stream
     for k, a in enumerate(range(0, flat.size, per)):
         b = min(flat.size, a + per)
         s = k & 1
@@ -564,10 +571,15 @@ def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20):
         step = max(1 << 16, -(-n // nthr))
         list(pool.map(lambda i: np.copyto(host[i:min(n, i + step)], flat[a + i:a + min(n, i + step)]),
                       range(0, n, step)))
-        dst[a:b].copy_(stage[s][:n], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        with torch.cuda.stream(copy):
+            dst[a:b].copy_(stage[s][:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
         done[s] = ev
+        compute.wait_event(ev)
+        if on_chunk is not None:
+            on_chunk(b)
+    out.record_stream(copy)
     return out
 
 
