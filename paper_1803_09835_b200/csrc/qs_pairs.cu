@@ -32,6 +32,7 @@
 //   MATCHED   emission only (occurrence-filter pass 1): screen on planes 0-7
 //   DISTINCT  distinct-pair count only (pass 2 after the filter)
 #include "qs_lsh.cuh"
+#include <cstdlib>
 
 namespace qs {
 
@@ -350,15 +351,26 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
     __syncwarp();
 }
 
-// Segmentation of a big bucket (s > L members): up to 2L members fit one
-// buffer as a single diagonal item; bigger buckets split into n_seg balanced
-// segments of <= L members, item (I, J), J >= I, pairing segments I and J.
-__host__ __device__ __forceinline__ uint32_t n_seg(uint32_t s, uint32_t L) {
-    return s <= 2 * L ? 1u : (s + L - 1) / L;
+// Items of a bucket of s > L members.  Up to 2L members fit one buffer as a
+// single item (all rows, every pair).  A bigger bucket is cut into 32-row A
+// groups g (rows [32g, 32g + 32)); each group pairs with the later rows
+// [32(g+1), s) in balanced B pieces of <= 2L - 32 rows, item (g, J), and the
+// group's first piece also carries its own triangle (a fold chunk).  Every
+// rectangular step then has a full 32-row A group except in the last group
+// (balanced I x J segments of <= L rows left lanes idle: 70 % lane use at cfg1).
+__host__ __device__ __forceinline__ uint32_t big_bmax(uint32_t L) { return 2 * L - 32; }
+__host__ __device__ __forceinline__ uint32_t g_pieces(uint32_t s, uint32_t g, uint32_t bmax) {
+    const uint32_t b0 = 32 * (g + 1);
+    return s > b0 ? (s - b0 + bmax - 1) / bmax : 1u;
 }
-__host__ __device__ __forceinline__ uint32_t seg_len(uint32_t s, uint32_t L) {
-    const uint32_t ns = n_seg(s, L);
-    return (s + ns - 1) / ns;
+__host__ __device__ __forceinline__ uint32_t big_groups(uint32_t s, uint32_t L) {
+    return s <= 2 * L ? 1u : (s + 31) / 32;
+}
+__host__ __device__ __forceinline__ uint64_t big_items(uint32_t s, uint32_t L) {
+    if (s <= 2 * L) return 1;
+    uint64_t c = 0;
+    for (uint32_t g = 0, ng = big_groups(s, L); g < ng; ++g) c += g_pieces(s, g, big_bmax(L));
+    return c;
 }
 
 // chunk descriptor: x = abase | bbeg << 16; y = bend | acnt << 16 | tri << 22 | table << 23
@@ -441,7 +453,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
     constexpr int NP = C::NP;
     constexpr uint32_t L = C::L;
 #ifndef QS_FOLD_MATCHED
-#define QS_FOLD_MATCHED 0
+#define QS_FOLD_MATCHED 1
 #endif
 #ifndef QS_FOLD_OFF
     constexpr bool FOLD = MODE != MODE_MATCHED || QS_FOLD_MATCHED;  // fold chunks for triangles
@@ -547,13 +559,13 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 if (lane == 0) s_nrows[ma] = tot;
             } else {
                 uint64_t bk;
-                uint32_t I, J;
+                uint32_t g, J;
                 if (use_table) {
                     const uint64_t e = plan.bigitems[item - n_tiles];
                     bk = e >> 24;
-                    I = (uint32_t)(e >> 12) & 0xFFFu;
+                    g = (uint32_t)(e >> 12) & 0xFFFu;
                     J = (uint32_t)e & 0xFFFu;
-                } else {  // giant buckets: decode (bucket, I, J) from the item prefix
+                } else {  // giant buckets: decode (bucket, g, J) from the item prefix
                     const uint64_t idx = item - n_tiles;
                     uint64_t lo = 0, hi = plan.totals[1];
                     while (hi - lo > 1) {
@@ -562,45 +574,54 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         else hi = mid;
                     }
                     bk = plan.bigb[lo];
-                    const uint64_t nseg = n_seg(bsize[bk], L);
-                    uint64_t rem = idx - plan.bigoff[lo], ii = 0;
-                    while (rem >= nseg - ii) {
-                        rem -= nseg - ii;
-                        ++ii;
+                    const uint32_t sb = bsize[bk];
+                    uint64_t rem = idx - plan.bigoff[lo];
+                    uint32_t gg = 0;
+                    if (sb > 2 * L) {
+                        while (rem >= g_pieces(sb, gg, big_bmax(L))) {
+                            rem -= g_pieces(sb, gg, big_bmax(L));
+                            ++gg;
+                        }
                     }
-                    I = (uint32_t)ii;
-                    J = (uint32_t)(ii + rem);
+                    g = gg;
+                    J = (uint32_t)rem;
                 }
                 const uint32_t s = bsize[bk];
                 const uint64_t st = bstart[bk];
-                const uint32_t sl = seg_len(s, L);
-                const uint32_t i0 = I * sl, nI = min(sl, s - i0);
-                const uint32_t j0 = J * sl, nJ = (J == I) ? 0 : min(sl, s - j0);
-                for (uint32_t r = lane; r < nI + nJ; r += 32) {
+                uint32_t a0 = 0, nA = s, j0 = 0, nB = 0;  // s <= 2L: the whole bucket
+                if (s > 2 * L) {
+                    a0 = 32 * g;
+                    nA = min(32u, s - a0);
+                    const uint32_t b0 = a0 + 32, lb = s > b0 ? s - b0 : 0;
+                    if (lb) {
+                        const uint32_t np = g_pieces(s, g, big_bmax(L)), pl = (lb + np - 1) / np;
+                        j0 = b0 + J * pl;
+                        nB = min(pl, s - j0);
+                    }
+                }
+                QS_DASSERT(nA + nB <= C::CAP);
+                for (uint32_t r = lane; r < nA + nB; r += 32) {
                     QS_DASSERT(r < C::CAP);
-                    cp_async4(ids + r, sids + st + (r < nI ? i0 + r : j0 + (r - nI)));
+                    cp_async4(ids + r, sids + st + (r < nA ? a0 + r : j0 + (r - nA)));
                 }
                 if (lane == 0) {
                     const uint32_t table = btab[bk];
                     uint32_t cbase = 0;
-                    if (J == I) {
-                        emit_chunks_tri(chunks, 0, 0, nI, table, FOLD);
-                        cbase = count_chunks_tri(nI, FOLD);
-                    } else {
-                        for (uint32_t c = 0; c * 32 < nI; ++c) {
-                            const uint32_t np = n_pieces(nI, nI + nJ);
-                            for (uint32_t kk = 0; kk < np; ++kk) {
-                                const uint32_t bb = nI + kk * BPIECE;
-                                chunks[cbase++] = make_chunk(c * 32, min(32u, nI - c * 32), bb,
-                                                             min(nI + nJ, bb + BPIECE), false, table);
-                            }
-                        }
+                    if (J == 0) {  // the whole bucket, or group g's own triangle
+                        emit_chunks_tri(chunks, 0, 0, nA, table, FOLD);
+                        cbase = count_chunks_tri(nA, FOLD);
                     }
+                    const uint32_t np = n_pieces(nA, nA + nB);
+                    for (uint32_t kk = 0; kk < np; ++kk) {
+                        const uint32_t bb = nA + kk * BPIECE;
+                        chunks[cbase++] = make_chunk(0, nA, bb, min(nA + nB, bb + BPIECE), false, table);
+                    }
+                    QS_DASSERT(cbase <= C::MAXCH);
                     s_nch[ma] = cbase;
                 }
                 cp_async_wait_all();
                 __syncwarp();
-                if (lane == 0) s_nrows[ma] = nI + nJ;
+                if (lane == 0) s_nrows[ma] = nA + nB;
             }
             __syncwarp();
         };
@@ -874,15 +895,303 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
     PROF_FLUSH(4)
 }
 
+// --------------------------------------------- small buckets (2 <= s <= 32)
+// A bucket of s <= 32 members is one warp's work as a fold: lane r holds
+// member r's tag planes in registers and meets member (r + d) mod s for
+// d = 1 .. s/2 through register shuffles (every pair once; at d = s/2 of an
+// even s only r < d).  Buckets are grouped by size class (planning below) so
+// one warp task packs q = 32 / s buckets of the same size: lanes j*s .. j*s+s-1
+// hold bucket j and every lane does useful work on every step.  The main
+// kernel's tiles would spend a 32-lane broadcast step per member of such a
+// bucket (cfg1: 60 ms of the MATCHED pass for 7 % of its pairs).
+constexpr uint32_t SMALL_MAX = 32;
+constexpr int SM_WARPS = 8;  // warps per CTA of k_pairs_small
+constexpr int SM_CLS = 2 + 3 * 34;  // u32 words of the class table (see k_small_prefix)
+
+// class table (u32): cnt[34] at 0, start[34] at 34 (bucket prefix by size),
+// tpre[34] at 68 (task prefix by size), cursor[34] at 102
+__global__ void k_small_count(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                              uint32_t tmax, uint64_t nb, uint32_t smin, uint32_t smax,
+                              uint32_t* __restrict__ cls) {
+    __shared__ uint32_t h[34];
+    if (threadIdx.x < 34) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = bsize[i];
+        if (s >= smin && s <= smax && btab[i] <= tmax) atomicAdd(&h[s], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 34 && h[threadIdx.x]) atomicAdd(&cls[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void k_small_prefix(uint32_t* __restrict__ cls) {
+    if (threadIdx.x != 0) return;
+    uint32_t acc = 0, tacc = 0;
+    for (uint32_t s = 0; s < 34; ++s) {
+        const uint32_t c = cls[s];
+        cls[34 + s] = acc;
+        cls[68 + s] = tacc;
+        cls[102 + s] = 0;
+        acc += c;
+        tacc += s >= 2 && s <= SMALL_MAX ? (c + 32 / s - 1) / (32 / s) : 0;
+    }
+    cls[34 + 33] = acc;  // start[33]: total small buckets (cnt[33] is always 0)
+    cls[68 + 33] = tacc;
+}
+
+// descriptor per small bucket, grouped by size: bstart | table << 48
+constexpr int SM_SCAT = 4;  // buckets per thread
+__global__ void __launch_bounds__(256) k_small_scatter(
+    const uint64_t* __restrict__ bstart, const uint32_t* __restrict__ bsize,
+    const uint32_t* __restrict__ btab, uint32_t tmax, uint64_t nb, uint32_t smin, uint32_t smax,
+    uint32_t* __restrict__ cls, uint64_t* __restrict__ desc) {
+    __shared__ uint32_t h[34], base[34];
+    if (threadIdx.x < 34) h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t i0 = (uint64_t)blockIdx.x * 256 * SM_SCAT + threadIdx.x;
+    uint32_t sz[SM_SCAT], rk[SM_SCAT];
+#pragma unroll
+    for (int k = 0; k < SM_SCAT; ++k) {
+        const uint64_t i = i0 + (uint64_t)k * 256;
+        sz[k] = 0;
+        if (i < nb) {
+            const uint32_t s = bsize[i];
+            if (s >= smin && s <= smax && btab[i] <= tmax) {
+                sz[k] = s;
+                rk[k] = atomicAdd(&h[s], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 34 && h[threadIdx.x]) base[threadIdx.x] = atomicAdd(&cls[102 + threadIdx.x], h[threadIdx.x]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SM_SCAT; ++k) {
+        if (!sz[k]) continue;
+        const uint64_t i = i0 + (uint64_t)k * 256;
+        const uint32_t pos = cls[34 + sz[k]] + base[sz[k]] + rk[k];
+        desc[pos] = bstart[i] | ((uint64_t)btab[i] << 48);
+    }
+}
+
+template <int W, int MODE, int WT>
+struct SmallCfg {  // tag-plane registers per lane -> CTAs per SM (register budget)
+    static constexpr int AREGS = Layout<MODE, WT>::off(W);
+    static constexpr int MINB = AREGS <= 36 ? 3 : 2;
+};
+
+// Per warp, tasks k, k + nw, ...: while task k's tag rows are loaded and
+// compared, the member ids of task k + nw and the descriptors of task k + 2nw
+// are already in flight, so only the row load of the dependent chain
+// descriptor -> member id -> tag row is exposed per task.
+template <int W, int MODE, bool HAS_E, int WT, bool EX>
+__global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) k_pairs_small(
+    const uint32_t* __restrict__ sids, const uint64_t* __restrict__ desc,
+    const uint32_t* __restrict__ cls, const uint64_t* __restrict__ rkeys,
+    const uint32_t* __restrict__ tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
+    const uint8_t* __restrict__ emask, const uint64_t* __restrict__ edges, uint32_t p,
+    uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim, uint32_t* __restrict__ out_rest,
+    uint64_t cap, unsigned long long* __restrict__ counters, uint32_t wg) {
+    using Lay = Layout<MODE, WT>;
+    constexpr int NP = TileCfg<W, MODE, WT>::NP;
+    constexpr int QW = QCAP * (3 + W);
+    __shared__ uint32_t s_start[34], s_tpre[34], s_q[34];
+    __shared__ uint16_t s_jr[34][32];  // (bucket j << 8 | member r) of lane l in class s
+    __shared__ uint32_t qsm[SM_WARPS][QW];
+    if (threadIdx.x < 34) {
+        s_start[threadIdx.x] = cls[34 + threadIdx.x];
+        s_tpre[threadIdx.x] = cls[68 + threadIdx.x];
+        s_q[threadIdx.x] = threadIdx.x >= 2 ? 32u / threadIdx.x : 0u;
+    }
+    for (uint32_t i = threadIdx.x; i < 34 * 32; i += blockDim.x) {
+        const uint32_t sc = i >> 5, l = i & 31;
+        s_jr[sc][l] = sc >= 2 ? (uint16_t)(((l / sc) << 8) | (l % sc)) : 0;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ntask = s_tpre[33];
+    const uint32_t nw = gridDim.x * SM_WARPS;
+    Queue q;
+    q.qa = qsm[warp];
+    q.qb = q.qa + QCAP;
+    q.qt = q.qb + QCAP;
+    q.qm = q.qt + QCAP;
+    uint32_t qhead = 0, qn = 0;
+    const uint32_t last_mask = (t & 31) ? ((1u << (t & 31)) - 1u) : 0xFFFFFFFFu;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    unsigned long long distinct = 0;
+
+    // task k -> packed geometry s | j << 6 | r << 11 | live << 16 (size class s,
+    // the lane's bucket j in the task and member r) and its descriptor slot
+    auto geom = [&](uint32_t k, uint32_t& pos) -> uint32_t {
+        const bool hit = k < ntask && lane >= 2 && s_tpre[lane] <= k && k < s_tpre[lane + 1];
+        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+        const uint32_t s = hb ? (uint32_t)(__ffs(hb) - 1) : 32u;
+        const uint32_t jr = s_jr[s][lane], j = jr >> 8, r = jr & 0xFF;
+        pos = k < ntask ? s_start[s] + (k - s_tpre[s]) * s_q[s] + j : 0u;
+        const bool live = k < ntask && j < s_q[s] && pos < s_start[s + 1];
+        return s | (j << 6) | (r << 11) | ((live ? 1u : 0u) << 16);
+    };
+    auto load_desc = [&](uint32_t k, uint32_t& g) -> uint64_t {
+        uint32_t pos;
+        g = geom(k, pos);
+        return (g >> 16) ? __ldg(desc + pos) : 0ull;
+    };
+    auto load_id = [&](uint32_t g, uint64_t d) -> uint32_t {
+        return (g >> 16) ? __ldg(sids + (d & 0xFFFFFFFFFFFFull) + ((g >> 11) & 31)) : 0u;
+    };
+
+    uint32_t k = blockIdx.x * SM_WARPS + warp;
+    uint32_t g0, g1;
+    uint64_t d0 = load_desc(k, g0), d1 = load_desc(k + nw, g1);
+    uint32_t a0 = load_id(g0, d0);
+    for (; k < ntask; k += nw) {
+        const uint32_t s = g0 & 63, j = (g0 >> 6) & 31, r = (g0 >> 11) & 31;
+        const bool live = (g0 >> 16) != 0;
+        const uint32_t a = a0;
+        uint32_t A[W][NP];
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+#pragma unroll
+            for (int qq = 0; qq < Lay::planes(w) / 4; ++qq) {
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (live)
+                    v = __ldg((const uint4*)(tags + ((uint64_t)(qq >> 1) * n + a) * wg * 8 + w * 8 +
+                                             (qq & 1) * 4));
+                A[w][qq * 4 + 0] = v.x; A[w][qq * 4 + 1] = v.y;
+                A[w][qq * 4 + 2] = v.z; A[w][qq * 4 + 3] = v.w;
+            }
+        // the next tasks' ids and descriptors go out with this task's rows
+        const uint32_t a1 = load_id(g1, d1);
+        uint32_t g2;
+        const uint64_t d2 = load_desc(k + 2 * nw, g2);
+        QS_DASSERT(!live || a < n);
+        const uint32_t table = (uint32_t)(d0 >> 48);
+        const uint32_t bt = table & 31, low = (1u << bt) - 1u;
+        const uint32_t tflag = (table & 0xFFu) | ((table >> 8) << 16);
+        const uint32_t half = s >> 1;
+        for (uint32_t dd = 1; dd <= half; ++dd) {
+            uint32_t rr = r + dd;
+            if (rr >= s) rr -= s;
+            const uint32_t src = live ? j * s + rr : lane;
+            const uint32_t bid = __shfl_sync(0xffffffffu, a, src);
+            // AND over np planes of ~(A ^ B) for word w, B = the partner's planes
+            auto maskw = [&](int w, int np) {
+                uint32_t x = 0xFFFFFFFFu;
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) {
+                    if (pp >= np) break;
+                    x &= ~(A[w][pp] ^ __shfl_sync(0xffffffffu, A[w][pp], src));
+                }
+                return x;
+            };
+            const uint32_t c = min(a, bid), qv = max(a, bid);
+            bool valid = live && (2 * dd != s || r < dd);
+            if (EX) valid = valid && (uint64_t)(qv - c) > excl;
+            if (HAS_E && valid) {
+                if (emask[c]) valid = false;
+                else if (emask[qv] && (p <= 1 || part_of(edges, p, qv) == part_of(edges, p, c)))
+                    valid = false;
+            }
+            bool slow = false;
+            uint32_t flags = tflag;
+            uint32_t qmask[W];
+            if (MODE == MODE_MATCHED) {
+                uint32_t cnt = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    uint32_t s8 = 0;
+                    if (w >= WT) {
+                        s8 = maskw(w, 8);
+                        if (w == (int)wg - 1) s8 &= last_mask;
+                        cnt += __popc(w == WT ? (s8 & ~((low << 1) | 1u)) : s8);
+                    }
+                    qmask[w] = s8;
+                }
+                slow = valid && cnt + 1 >= m;
+                flags |= QF_COUNT;
+            } else {
+                uint32_t early = 0, cnt = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    uint32_t x = 0;
+                    if (w <= WT) {
+                        x = maskw(w, Lay::planes(w));
+                        if (w == (int)wg - 1) x &= last_mask;
+                        early |= (w < WT) ? x : (x & low);
+                        if (w == WT) cnt += __popc(x & ~low);
+                    } else if (MODE == MODE_FULL) {
+                        x = maskw(w, 8);
+                        if (w == (int)wg - 1) x &= last_mask;
+                        cnt += __popc(x);
+                    }
+                    qmask[w] = x;
+                }
+                const bool need_count = (MODE == MODE_FULL) && cnt >= m;
+                if (valid) {
+                    if (early) {
+                        slow = true;
+                        flags |= QF_DISTINCT | (need_count ? QF_COUNT : 0u);
+                    } else {
+                        ++distinct;
+                        if (need_count) {
+                            slow = true;
+                            flags |= QF_COUNT;
+                        }
+                    }
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, slow);
+            if (bal) {
+                if (MODE == MODE_MATCHED) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w)
+                        if (w < WT) qmask[w] = maskw(w, 8);
+                }
+                if (slow) {
+                    const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
+                    QS_DASSERT(e < QCAP && c < qv && qv < n);
+                    q.qa[e] = c;
+                    q.qb[e] = qv;
+                    q.qt[e] = flags;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) q.qm[e * W + w] = qmask[w];
+                }
+                qn += __popc(bal);
+                if (qn >= 32) {
+                    __syncwarp();
+                    drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
+                             counters, distinct);
+                    qhead = (qhead + 32) & (QCAP - 1);
+                    qn -= 32;
+                }
+            }
+        }
+        g0 = g1; g1 = g2;
+        d0 = d1; d1 = d2;
+        a0 = a1;
+    }
+    __syncwarp();
+    if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
+                     distinct);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
+    if (lane == 0 && distinct) atomicAdd(counters + 0, distinct);
+}
+
 // --------------------------------------------------------------- planning
 // buckets of tables > tmax are left out (MATCHED: a pair with sim >= m has its
 // first collision in a table <= t - m)
+// (smin, smax: a bucket-size window, a design-measurement knob; 0, ~0 = all)
 __global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
                              uint32_t tmax, uint64_t nb, uint32_t L,
-                             uint64_t* __restrict__ small, uint64_t* __restrict__ bigflag) {
+                             uint64_t* __restrict__ small, uint64_t* __restrict__ bigflag,
+                             uint32_t smin, uint32_t smax) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = (i < nb && btab[i] <= tmax) ? bsize[i] : 0;
+        uint32_t s = (i < nb && btab[i] <= tmax) ? bsize[i] : 0;
+        if (s < smin || s > smax) s = 0;
         small[i] = (i < nb && s <= L) ? s : 0;
         bigflag[i] = (i < nb && s > L) ? 1 : 0;
     }
@@ -892,17 +1201,17 @@ __global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, const uint32_t*
 __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
                            uint32_t tmax, uint64_t nb, uint32_t L,
                            const uint64_t* __restrict__ bigpos, uint64_t* __restrict__ bigb,
-                           uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg) {
+                           uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg,
+                           uint32_t smin, uint32_t smax) {
     uint32_t mx = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = bsize[i];
-        if (s <= L || btab[i] > tmax) continue;
+        if (s <= L || btab[i] > tmax || s < smin || s > smax) continue;
         const uint64_t k = bigpos[i];
-        const uint64_t nseg = n_seg(s, L);
         bigb[k] = i;
-        bigcnt[k] = nseg * (nseg + 1) / 2;
-        mx = max(mx, (uint32_t)nseg);
+        bigcnt[k] = big_items(s, L);
+        mx = max(mx, big_groups(s, L));
     }
     // one atomic per warp (a single contended address otherwise serialises)
 #pragma unroll
@@ -918,10 +1227,12 @@ __global__ void k_plan_bigitems(const uint32_t* __restrict__ bsize, const uint64
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nbig;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = bigb[k];
-        const uint32_t nseg = n_seg(bsize[b], L);
+        const uint32_t sb = bsize[b], ng = big_groups(sb, L);
         uint64_t o = bigoff[k];
-        for (uint32_t I = 0; I < nseg; ++I)
-            for (uint32_t J = I; J < nseg; ++J) items[o++] = (b << 24) | ((uint64_t)I << 12) | J;
+        for (uint32_t g = 0; g < ng; ++g) {
+            const uint32_t np = sb > 2 * L ? g_pieces(sb, g, big_bmax(L)) : 1u;
+            for (uint32_t J = 0; J < np; ++J) items[o++] = (b << 24) | ((uint64_t)g << 12) | J;
+        }
     }
 }
 
@@ -1046,7 +1357,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
                   uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
                   const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
                   uint32_t* out_rest, uint64_t cap, unsigned long long* counters, uint64_t* ws,
-                  void* sws, cudaStream_t st, uint32_t wg) {
+                  void* sws, void* smws, cudaStream_t st, uint32_t wg) {
     using C = TileCfg<W, MODE, WT>;
     const uint32_t L = C::L;
     uint64_t* mpre = ws;                       // nb + 1
@@ -1060,7 +1371,35 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     const uint64_t items_cap = (nb + 1) * 8;
     const unsigned g = qs_blocks(nb + 1, 256);
     const uint32_t tmax = MODE == MODE_MATCHED ? t - m : t - 1;
-    k_plan_sizes<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, mpre, bigpos);
+    const uint32_t smin_env = getenv("QS_PAIRS_SMIN") ? (uint32_t)atoi(getenv("QS_PAIRS_SMIN")) : 0u;
+    const uint32_t smax = getenv("QS_PAIRS_SMAX") ? (uint32_t)atoi(getenv("QS_PAIRS_SMAX")) : ~0u;
+    // buckets of <= SMALL_MAX members go to k_pairs_small (QS_SMALL=0: all to k_pairs_pc)
+    static const bool small_on = !getenv("QS_SMALL") || atoi(getenv("QS_SMALL")) != 0;
+    uint32_t smin = smin_env;
+    if (small_on) {
+        uint32_t* cls = (uint32_t*)smws;
+        uint64_t* desc = (uint64_t*)((char*)smws + 1024);
+        const uint32_t lo = max(2u, smin_env), hi = min(SMALL_MAX, smax);
+        smin = max(smin_env, SMALL_MAX + 1);
+        if (lo <= hi) {
+            QS_CUDA(cudaMemsetAsync(cls, 0, SM_CLS * 4, st), "memset");
+            k_small_count<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, lo, hi, cls);
+            k_small_prefix<<<1, 32, 0, st>>>(cls);
+            k_small_scatter<<<(unsigned)((nb + 256 * SM_SCAT - 1) / (256 * SM_SCAT)), 256, 0, st>>>(
+                bstart, bsize, btab, tmax, nb, lo, hi, cls, desc);
+            auto sk = excl > 0 ? k_pairs_small<W, MODE, HAS_E, WT, true>
+                               : k_pairs_small<W, MODE, HAS_E, WT, false>;
+            constexpr size_t ssm = 0;
+            int per_sm_s = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, sk, SM_WARPS * 32, ssm);
+            if (per_sm_s < 1) per_sm_s = 1;
+            sk<<<num_sms() * per_sm_s, SM_WARPS * 32, ssm, st>>>(sids, desc, cls, rkeys, tags, n, t, m,
+                                                             excl, emask, edges, p, out_key, out_sim,
+                                                             out_rest, cap, counters, wg);
+            QS_CHECK_LAUNCH("k_pairs_small");
+        }
+    }
+    k_plan_sizes<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, mpre, bigpos, smin, smax);
     int rc = scan_u64(mpre, mpre, nb + 1, totals + 0, sws, st);
     if (rc) return rc;
     rc = scan_u64(bigpos, bigpos, nb + 1, totals + 1, sws, st);
@@ -1068,7 +1407,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     QS_CUDA(cudaMemsetAsync(bigoff, 0, (nb + 1) * 8, st), "memset");
     QS_CUDA(cudaMemsetAsync(totals + 4, 0, 8, st), "memset");
     k_plan_big<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, bigpos, bigb, bigoff,
-                                  (unsigned long long*)(totals + 4));
+                                  (unsigned long long*)(totals + 4), smin, smax);
     rc = scan_u64(bigoff, bigoff, nb + 1, nullptr, sws, st);
     if (rc) return rc;
     k_plan_tiles<<<g, 256, 0, st>>>(mpre, nb, L, totals, bigoff, tile_first, items_cap);
@@ -1114,7 +1453,8 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
                           const uint32_t* tags, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
                           const uint8_t* emask, const uint64_t* edges, uint32_t p, uint64_t* ok,
                           uint32_t* os, uint32_t* orest, uint64_t cap,
-                          unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
+                          unsigned long long* counters, uint64_t* ws, void* sws, void* smws,
+                          cudaStream_t st) {
     uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
     k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
     uint64_t hb[5] = {0, 0, 0, 0, 0};
@@ -1127,7 +1467,7 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
 #define QS_W(WW, WTT)                                                                             \
     run_pc<WW, MODE, HAS_E, WTT>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
                                  m, excl, emask, edges, p, ok, os, orest, cap, counters, ws, sws, \
-                                 st, W)
+                                 smws, st, W)
         constexpr bool DI = MODE == MODE_DISTINCT;
         int rc = QS_OK;
         if (w == 0) {
@@ -1151,18 +1491,15 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
                          const uint64_t* rkeys, const uint32_t* tags, uint64_t n, uint32_t t,
                          uint32_t m, uint64_t excl, const uint8_t* emask, const uint64_t* edges,
                          uint32_t p, uint64_t* ok, uint32_t* os, uint32_t* orest, uint64_t cap,
-                         unsigned long long* counters, uint64_t* ws, void* sws, cudaStream_t st) {
-#define QS_L(MM, EE) \
-    run_pc<W, MM, EE, 0>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, edges, \
-                         p, ok, os, orest, cap, counters, ws, sws, st, W)
+                         unsigned long long* counters, uint64_t* ws, void* sws, void* smws,
+                         cudaStream_t st) {
 #define QS_D(MM, EE) \
     run_word_split<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
-                              edges, p, ok, os, orest, cap, counters, ws, sws, st)
+                              edges, p, ok, os, orest, cap, counters, ws, sws, smws, st)
     if (mode != MODE_MATCHED) orest = nullptr;  // lazy counts: MATCHED only
     if (mode == MODE_FULL) return has_e ? QS_D(MODE_FULL, true) : QS_D(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_D(MODE_MATCHED, true) : QS_D(MODE_MATCHED, false);
     return has_e ? QS_D(MODE_DISTINCT, true) : QS_D(MODE_DISTINCT, false);
-#undef QS_L
 #undef QS_D
 }
 
@@ -1206,7 +1543,9 @@ int qs_prof_read(unsigned long long* out, int reset) {
 // member-bucket slot for s <= 4L; larger buckets are bounded by the member
 // count (s / L items per segment row), so 8 slots per bucket bound the table.
 size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle) {
-    return (size_t)(n_nonsingle + 1) * 8 * (5 + 8) + 64 + scan_ws_bytes(n_nonsingle + 1) + 512;
+    // + the small-bucket class table (1 KB) and descriptors (8 B per bucket)
+    return (size_t)(n_nonsingle + 1) * 8 * (5 + 8) + 64 + scan_ws_bytes(n_nonsingle + 1) + 512 +
+           1024 + (size_t)(n_nonsingle + 1) * 8 + 64;
 }
 
 int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
@@ -1223,12 +1562,13 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
     const uint64_t nb = n_nonsingle;
     uint64_t* ws = (uint64_t*)ws_dev;
     void* sws = (void*)(((uintptr_t)(ws + (nb + 1) * 13 + 8) + 63) & ~(uintptr_t)63);
+    void* smws = (void*)(((uintptr_t)sws + scan_ws_bytes(nb + 1) + 63) & ~(uintptr_t)63);
     const uint32_t W = (t + 31) >> 5;
     const bool has_e = excluded_dev != nullptr;
 #define QS_D(WW)                                                                                  \
     dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, nb, rkeys_dev,      \
                       tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,           \
-                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, st)
+                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, smws, st)
     switch (W) {
         case 1: return QS_D(1);
         case 2: return QS_D(2);
