@@ -225,6 +225,14 @@ __device__ __forceinline__ uint32_t confirm(const uint64_t* __restrict__ rkeys, 
     uint32_t hits = 0;
     const uint64_t* ra = rkeys + (uint64_t)a * t + wbase;
     const uint64_t* rb = rkeys + (uint64_t)b * t + wbase;
+    if (stop_first && cand) {
+        // the lowest candidate alone first: for a pair that is not first in
+        // this bucket it is usually a true collision, and the other three key
+        // pairs of a batch would be wasted random reads
+        const uint32_t t0 = (uint32_t)(__ffs(cand) - 1);
+        if (__ldg(ra + t0) == __ldg(rb + t0)) return 1;
+        cand &= cand - 1;
+    }
     while (cand) {
         uint32_t tt[4];
         bool v[4];
