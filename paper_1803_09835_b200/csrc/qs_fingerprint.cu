@@ -704,11 +704,11 @@ constexpr uint32_t WC_N = 2048, WC_T64 = 64;
 constexpr uint32_t WC_FT = 2, WC_TT = 3, WC_NWID = 3;
 constexpr uint64_t WC_SIGN = 1ull << 63;
 // shared layout (bytes): keys u64[2048] (band rows alias it before the Haar) |
-// tmp f64[64 * 16] (candidate lists alias it after level 1) | ll1 f64[512] |
+// tmp f64[16][64] (the select histograms alias it after level 1) | ll1 f64[512] |
 // ll2 f64[128] | level-3+ coefficients f32[128] | hist u32[256] | tables
 constexpr size_t WC_OFF_TMP = WC_N * 8, WC_OFF_LL1 = WC_OFF_TMP + 64 * 16 * 8;
 constexpr size_t WC_OFF_LL2 = WC_OFF_LL1 + 512 * 8, WC_OFF_LL3 = WC_OFF_LL2 + 128 * 8;
-constexpr size_t WC_OFF_HIST = WC_OFF_LL3 + 64 * 8, WC_OFF_TAB = WC_OFF_HIST + 256 * 4;
+constexpr size_t WC_OFF_TAB = WC_OFF_LL3 + 64 * 8;
 constexpr size_t WC_SMEM = WC_OFF_TAB + (32 * WC_FT + WC_NWID * 64 * WC_TT) * 12 + 64;
 
 __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
@@ -722,18 +722,15 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
     uint64_t* keys = (uint64_t*)csm;
     float* gs = (float*)csm;
     double* tmp = (double*)(csm + WC_OFF_TMP);
-    uint16_t* la = (uint16_t*)tmp;
-    uint16_t* lb = la + WC_N;
     double* ll1 = (double*)(csm + WC_OFF_LL1);
     double* ll2 = (double*)(csm + WC_OFF_LL2);
     double* ll3 = (double*)(csm + WC_OFF_LL3);
-    uint32_t* hist = (uint32_t*)(csm + WC_OFF_HIST);
     double* fv = (double*)(csm + WC_OFF_TAB);
     double* tv = fv + 32 * WC_FT;
     int32_t* fi = (int32_t*)(tv + WC_NWID * 64 * WC_TT);
     int32_t* ti = fi + 32 * WC_FT;
     __shared__ uint32_t s_nf, s_wcnt[WC_W], s_wcnt2[WC_W], s_ncur;
-    __shared__ uint32_t s_dsel, s_krem, s_gt;
+    __shared__ uint32_t s_dsel;
     __shared__ uint64_t s_kmax, s_kmin;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
     const uint32_t nwid = g.wmax - g.wmin + 1, nb = g.nb, mode = g.mode;
@@ -754,11 +751,22 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         ti[q] = ok ? wt_idx[e] : 0;
     }
     const double s2 = 0.7071067811865475;  // 1.0 / math.sqrt(2.0), as the reference
+    // window columns: c0 = ceil(idx * lag / hop), c1 = (idx * lag + win - frame) / hop + 1;
+    // when hop divides lag (the BASELINE geometry) both are idx * (lag / hop) + constants
+    const uint64_t lh = g.lag / g.hop;
+    const bool lag_exact = lh * g.hop == g.lag;
+    const uint64_t wfix = (g.win - g.frame) / g.hop + 1;
     for (uint64_t wi = blockIdx.x; wi < g.n_win; wi += gridDim.x) {
         const uint64_t idx = widx ? (uint64_t)widx[wi] : g.win0 + wi;
-        const uint64_t off = idx * g.lag;
-        const uint64_t c0 = (off + g.hop - 1) / g.hop;
-        const uint64_t c1 = (off + g.win - g.frame) / g.hop + 1;
+        uint64_t c0, c1;
+        if (lag_exact) {
+            c0 = idx * lh;
+            c1 = c0 + wfix;
+        } else {
+            const uint64_t off = idx * g.lag;
+            c0 = (off + g.hop - 1) / g.hop;
+            c1 = (off + g.win - g.frame) / g.hop + 1;
+        }
         const uint32_t width = (uint32_t)(c1 - c0);
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -771,8 +779,8 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         // time resample (f64, CSR order; padded taps add exact zeros)
         const double* tvw = tv + (uint64_t)(width - g.wmin) * 64 * WC_TT;
         const int32_t* tiw = ti + (uint64_t)(width - g.wmin) * 64 * WC_TT;
-        for (uint32_t i = threadIdx.x; i < 64 * nb; i += WC_T) {
-            const uint32_t Ti = i / nb, f = i - Ti * nb;
+        for (uint32_t i = threadIdx.x; i < 64 * nb; i += WC_T) {  // tmp[f][Ti], f-major
+            const uint32_t Ti = i & 63, f = i >> 6;
             double acc = 0.0;
 #pragma unroll
             for (uint32_t t = 0; t < WC_TT; ++t)
@@ -824,7 +832,7 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const uint32_t c = 2 * bj + b;
-                    const double acc = fma(w1, tmp[c * nb + i1], fma(w0, tmp[c * nb + i0], 0.0));
+                    const double acc = fma(w1, tmp[i1 * 64 + c], fma(w0, tmp[i0 * 64 + c], 0.0));
                     x[a][b] = (double)(float)acc;  // images are float32 (fingerprint.py:239-241)
                 }
             }
@@ -884,6 +892,11 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
             const uint32_t j = (threadIdx.x >> 4) * 64 + (threadIdx.x & 15);
             emit(j, (double)c3[threadIdx.x]);
         }
+        // select histograms (3 x 256, triple-buffered) and the <= 32-candidate
+        // list live in the time-resample scratch, free after level 1
+        uint32_t* H = (uint32_t*)tmp;
+        uint64_t* clist = (uint64_t*)(H + 3 * 256);
+        H[threadIdx.x] = 0;
         // CTA-wide non-finite flag, key range
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -904,34 +917,41 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         }
         kmax = s_kmax;
         kmin = s_kmin;
+        // each thread's 8 keys (j = 256 w + 32 q + lane) stay in registers for
+        // the select passes and the emission
+        uint64_t kr[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) kr[q] = keys[256 * warp + 32 * q + lane];
         // 8-bit digits starting at the highest bit where the eligible keys
         // differ (bits above it are common to all of them); the last digit may
-        // overlap decided bits (constant over the candidates)
+        // overlap decided bits (constant over the candidates).  Pass p counts
+        // into histogram p % 3 and clears histogram (p + 1) % 3, last read by
+        // pass p - 2: one barrier per pass.  Once <= 32 candidates share the
+        // decided prefix, one warp ranks them.
         const uint64_t dk = kmax ^ kmin;
         int shift = dk ? max(0, 63 - __clzll((long long)dk) - 7) : 0;
         uint64_t decided = shift + 8 < 64 ? ~0ull << (shift + 8) : 0ull;
         uint64_t prefix = kmax & decided;
-        uint32_t krem = g.top_k, ncur = WC_N, gt = 0;
-        bool full = true;
-        uint16_t* cur = la;
-        uint16_t* nxt = lb;
-        bool done = false;
-        for (;;) {
-            for (uint32_t i = threadIdx.x; i < 256; i += WC_T) hist[i] = 0;
-            __syncthreads();
-            const uint64_t hmask = decided;
-            for (uint32_t jj = threadIdx.x; jj < ncur; jj += WC_T) {
-                const uint64_t k = keys[full ? jj : cur[jj]] & ~WC_SIGN;
-                if (k && (k & hmask) == prefix) atomicAdd(&hist[(uint32_t)(k >> shift) & 0xFFu], 1u);
+        uint32_t krem = g.top_k, gt = 0;
+        uint64_t thr = 0;
+        for (uint32_t pass = 0;; ++pass) {
+            uint32_t* hc = H + (pass % 3) * 256;
+            uint32_t* hn = H + ((pass + 1) % 3) * 256;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint64_t k = kr[q] & ~WC_SIGN;
+                if (k && (k & decided) == prefix) atomicAdd(&hc[(uint32_t)(k >> shift) & 0xFFu], 1u);
             }
+            hn[threadIdx.x] = 0;
             if (threadIdx.x == 0) s_ncur = 0;
             __syncthreads();
-            // every warp finds the digit holding the krem-th largest (no extra barrier)
+            // every warp finds the digit holding the krem-th largest
+            uint32_t csel;
             {
                 uint32_t c[8], sum = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    c[e] = hist[8 * lane + e];
+                    c[e] = hc[8 * lane + e];
                     sum += c[e];
                 }
                 uint32_t x = sum;
@@ -942,12 +962,13 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
                 }
                 const uint32_t above = x - sum;
                 const bool mine = above < krem && krem <= x;
-                uint32_t cum = above, dsel = 8 * lane;
+                uint32_t cum = above, dsel = 8 * lane, cs = 0;
                 if (mine) {
 #pragma unroll
                     for (int e = 7; e >= 0; --e) {
                         if (cum + c[e] >= krem) {
                             dsel = 8 * lane + e;
+                            cs = c[e];
                             break;
                         }
                         cum += c[e];
@@ -956,40 +977,30 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
                 const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
                 dsel = __shfl_sync(0xffffffffu, dsel, owner);
                 cum = __shfl_sync(0xffffffffu, cum, owner);
+                csel = __shfl_sync(0xffffffffu, cs, owner);
                 krem -= cum;
                 gt += cum;
                 prefix = (prefix & ~(0xFFull << shift)) | ((uint64_t)dsel << shift);
                 decided |= 0xFFull << shift;
             }
-            if (shift == 0) break;
-            // keep the matching candidates (order is irrelevant for the select)
-            const uint64_t kmask = decided;
-            for (uint32_t j0 = 0; j0 < ncur; j0 += WC_T) {
-                const uint32_t jj = j0 + threadIdx.x;
-                bool keep = false;
-                uint32_t j = 0;
-                if (jj < ncur) {
-                    j = full ? jj : cur[jj];
-                    const uint64_t k = keys[j] & ~WC_SIGN;
-                    keep = k && (k & kmask) == prefix;
-                }
-                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-                uint32_t wb = 0;
-                if (lane == 0 && bal) wb = atomicAdd(&s_ncur, __popc(bal));
-                wb = __shfl_sync(0xffffffffu, wb, 0);
-                if (keep) nxt[wb + __popc(bal & lt)] = (uint16_t)j;
+            if (shift == 0) {
+                thr = prefix;
+                break;
             }
-            __syncthreads();
-            ncur = s_ncur;
-            uint16_t* t2 = cur; cur = nxt; nxt = t2;
-            full = false;
             shift = shift >= 8 ? shift - 8 : 0;
-            if (ncur <= 32) {  // the rest by ranks inside one warp
+            if (csel <= 32) {  // the rest by ranks inside one warp
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint64_t k = kr[q] & ~WC_SIGN;
+                    if (k && (k & decided) == prefix) clist[atomicAdd(&s_ncur, 1u)] = k;
+                }
+                __syncthreads();
                 if (warp == 0) {
-                    const uint64_t k = lane < ncur ? keys[cur[lane]] & ~WC_SIGN : 0ull;
+                    const uint32_t ncur = s_ncur;
+                    const uint64_t k = lane < ncur ? clist[lane] : 0ull;
                     uint32_t greater = 0, geq = 0;
-                    for (uint32_t m = 0; m < ncur; ++m) {
-                        const uint64_t km = __shfl_sync(0xffffffffu, k, m);
+                    for (uint32_t mm = 0; mm < ncur; ++mm) {
+                        const uint64_t km = __shfl_sync(0xffffffffu, k, mm);
                         greater += km > k;
                         geq += km >= k;
                     }
@@ -1001,21 +1012,18 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
                     }
                 }
                 __syncthreads();
-                prefix = s_kmax;
+                thr = s_kmax;
                 gt += s_dsel;
-                done = true;
                 break;
             }
         }
-        (void)done;
-        const uint64_t thr = prefix;
         const uint32_t need = g.top_k - gt;
         // emission in index order: warp w owns key words 8w .. 8w + 7 (keys
         // 256 w .. 256 w + 255); per-warp counts of ties and takes, then prefixes
         uint32_t beqs[8], ntie = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const uint64_t k = keys[256 * warp + 32 * q + lane] & ~WC_SIGN;
+            const uint64_t k = kr[q] & ~WC_SIGN;
             beqs[q] = __ballot_sync(0xffffffffu, k == thr);
             ntie += __popc(beqs[q]);
         }
@@ -1026,7 +1034,7 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         uint32_t takes[8], ntake = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const uint64_t k = keys[256 * warp + 32 * q + lane] & ~WC_SIGN;
+            const uint64_t k = kr[q] & ~WC_SIGN;
             const bool take = k > thr || (k == thr && eqseen + __popc(beqs[q] & lt) < need);
             takes[q] = __ballot_sync(0xffffffffu, take);
             ntake += __popc(takes[q]);
@@ -1041,7 +1049,7 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         for (int q = 0; q < 8; ++q) {
             const uint32_t j = 256 * warp + 32 * q + lane;
             if ((takes[q] >> lane) & 1u)
-                ob[pos + __popc(takes[q] & lt)] = 2 * j + (uint32_t)(keys[j] >> 63);
+                ob[pos + __popc(takes[q] & lt)] = 2 * j + (uint32_t)(kr[q] >> 63);
             pos += __popc(takes[q]);
         }
     }
