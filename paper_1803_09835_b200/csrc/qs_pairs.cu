@@ -882,6 +882,26 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
             } else {
                 uint32_t u = bbeg;
                 const uint32_t* R = rows + bbeg * C::ROWP;
+#ifndef QS_PAIR_UNROLL2
+#define QS_PAIR_UNROLL2 1
+#endif
+#if QS_PAIR_UNROLL2
+                // DISTINCT: two rows per iteration, their independent mask chains
+                // interleave (-2 to -3 ms per bucket-size class at cfg1; the MATCHED
+                // pass at its 96-register cap gets slower: 220 -> 294 ms)
+#ifndef QS_UNROLL_MATCHED
+#define QS_UNROLL_MATCHED 0
+#endif
+                if (MODE == MODE_DISTINCT || (MODE == MODE_MATCHED && QS_UNROLL_MATCHED))
+                for (; u + 1 < bend; u += 2, R += 2 * C::ROWP) {
+                    bool s0, s1;
+                    uint32_t f0, f1, m0[W], m1[W];
+                    eval(u, R, false, false, s0, f0, m0);
+                    eval(u + 1, R + C::ROWP, false, false, s1, f1, m1);
+                    push(u, R, false, s0, f0, m0);
+                    push(u + 1, R + C::ROWP, false, s1, f1, m1);
+                }
+#endif
                 for (; u < bend; ++u, R += C::ROWP) {
                     bool s0;
                     uint32_t f0, m0[W];
