@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(256) k_small_scatter(
 template <int W, int MODE, int WT>
 struct SmallCfg {  // tag-plane registers per lane -> CTAs per SM (register budget)
     static constexpr int AREGS = Layout<MODE, WT>::off(W);
-    static constexpr int MINB = AREGS <= 36 ? 3 : 2;
+    static constexpr int MINB = 2;
 };
 
 // Per warp, tasks k, k + nw, ...: while task k's tag rows are loaded and
@@ -1070,30 +1070,40 @@ __global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) 
         return (g >> 16) ? __ldg(sids + (d & 0xFFFFFFFFFFFFull) + ((g >> 11) & 31)) : 0u;
     };
 
-    uint32_t k = blockIdx.x * SM_WARPS + warp;
-    uint32_t g0, g1;
-    uint64_t d0 = load_desc(k, g0), d1 = load_desc(k + nw, g1);
-    uint32_t a0 = load_id(g0, d0);
-    for (; k < ntask; k += nw) {
-        const uint32_t s = g0 & 63, j = (g0 >> 6) & 31, r = (g0 >> 11) & 31;
-        const bool live = (g0 >> 16) != 0;
-        const uint32_t a = a0;
-        uint32_t A[W][NP];
+    // the lane's tag planes of member `id` (zeros for a dead lane)
+    auto load_rows = [&](uint32_t (&X)[W][NP], uint32_t id, uint32_t g) {
 #pragma unroll
         for (int w = 0; w < W; ++w)
 #pragma unroll
             for (int qq = 0; qq < Lay::planes(w) / 4; ++qq) {
                 uint4 v = make_uint4(0, 0, 0, 0);
-                if (live)
-                    v = __ldg((const uint4*)(tags + ((uint64_t)(qq >> 1) * n + a) * wg * 8 + w * 8 +
+                if (g >> 16)
+                    v = __ldg((const uint4*)(tags + ((uint64_t)(qq >> 1) * n + id) * wg * 8 + w * 8 +
                                              (qq & 1) * 4));
-                A[w][qq * 4 + 0] = v.x; A[w][qq * 4 + 1] = v.y;
-                A[w][qq * 4 + 2] = v.z; A[w][qq * 4 + 3] = v.w;
+                X[w][qq * 4 + 0] = v.x; X[w][qq * 4 + 1] = v.y;
+                X[w][qq * 4 + 2] = v.z; X[w][qq * 4 + 3] = v.w;
             }
-        // the next tasks' ids and descriptors go out with this task's rows
-        const uint32_t a1 = load_id(g1, d1);
-        uint32_t g2;
-        const uint64_t d2 = load_desc(k + 2 * nw, g2);
+    };
+
+    uint32_t k = blockIdx.x * SM_WARPS + warp;
+    uint32_t g0, g1, g2;
+    uint64_t d0 = load_desc(k, g0), d1 = load_desc(k + nw, g1);
+    uint32_t a0 = load_id(g0, d0);
+    uint32_t A[W][NP];
+    load_rows(A, a0, g0);
+    uint32_t a1 = load_id(g1, d1);
+    uint64_t d2 = load_desc(k + 2 * nw, g2);
+    for (; k < ntask; k += nw) {
+        const uint32_t s = g0 & 63, j = (g0 >> 6) & 31, r = (g0 >> 11) & 31;
+        const bool live = (g0 >> 16) != 0;
+        const uint32_t a = a0;
+        // the next task's rows, ids and descriptors are in flight while this
+        // task's pairs are compared
+        uint32_t An[W][NP];
+        load_rows(An, a1, g1);
+        const uint32_t a2 = load_id(g2, d2);
+        uint32_t g3;
+        const uint64_t d3 = load_desc(k + 3 * nw, g3);
         QS_DASSERT(!live || a < n);
         const uint32_t table = (uint32_t)(d0 >> 48);
         const uint32_t bt = table & 31, low = (1u << bt) - 1u;
@@ -1196,9 +1206,13 @@ __global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) 
                 }
             }
         }
-        g0 = g1; g1 = g2;
-        d0 = d1; d1 = d2;
-        a0 = a1;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+#pragma unroll
+            for (int pp = 0; pp < NP; ++pp) A[w][pp] = An[w][pp];
+        g0 = g1; g1 = g2; g2 = g3;
+        d0 = d1; d1 = d2; d2 = d3;
+        a0 = a1; a1 = a2;
     }
     __syncwarp();
     if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
