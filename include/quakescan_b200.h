@@ -206,6 +206,32 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                  uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
                  void* stream);
 
+/* qs_lsh_pairs restricted to the buckets of table words [word_lo, word_hi)
+ * (table word = table / 32; t <= 128).  core_count_dev (mode 1 only, may be
+ * NULL): the member lists are core-first (qs_lsh_core_first) and bucket b's
+ * first core_count_dev[b] members are fingerprints already known to exceed
+ * the occurrence limit; pairs of two of them are skipped — they change no
+ * output of the occurrence-filtered search (partitions == 1): both endpoints
+ * are core, hence excluded, whatever their count (lsh_search.py:256-287). */
+int qs_lsh_pairs_ex(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                    const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t n_nonsingle,
+                    const uint64_t* rkeys_dev, const uint32_t* tags_dev, uint64_t n, uint32_t t,
+                    uint32_t m, uint64_t excl, const uint8_t* excluded_dev,
+                    const uint64_t* edges_dev, uint32_t p, int mode,
+                    uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
+                    uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
+                    uint32_t word_lo, uint32_t word_hi, const uint32_t* core_count_dev,
+                    void* stream);
+
+/* Core-first member lists for qs_lsh_pairs_ex: for every bucket of a table
+ * >= table_lo, a stable partition of its ids (core_dev[id] != 0 first) into
+ * sids_out_dev at the same positions, and the number of core members in
+ * core_count_dev[b] (0 for buckets of earlier tables, which are not copied). */
+int qs_lsh_core_first(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                      const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t n_nonsingle,
+                      uint32_t table_lo, const uint8_t* core_dev, uint32_t* sids_out_dev,
+                      uint32_t* core_count_dev, void* stream);
+
 /* Exact counts of lazily counted pairs (see qs_lsh_pairs): pair_sim_dev[i] +=
  * the agreeing tables among rest_dev[i * ceil(t/32) ...]. */
 int qs_lsh_complete_sims(const uint64_t* pair_key_dev, uint32_t* pair_sim_dev,

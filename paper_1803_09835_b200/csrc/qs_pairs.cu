@@ -366,18 +366,33 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
 // group's first piece also carries its own triangle (a fold chunk).  Every
 // rectangular step then has a full 32-row A group except in the last group
 // (balanced I x J segments of <= L rows left lanes idle: 70 % lane use at cfg1).
+//
+// Core-first lists (MATCHED passes after the first table word, occurrence
+// filter on): the bucket's nc members known to be core are listed first and
+// pairs of two of them are skipped (they change no output: both endpoints are
+// excluded whatever their count).  A group wholly inside the core prefix keeps
+// only the B rows >= nc and no triangle; every other group is unchanged.
 __host__ __device__ __forceinline__ uint32_t big_bmax(uint32_t L) { return 2 * L - 32; }
-__host__ __device__ __forceinline__ uint32_t g_pieces(uint32_t s, uint32_t g, uint32_t bmax) {
-    const uint32_t b0 = 32 * (g + 1);
-    return s > b0 ? (s - b0 + bmax - 1) / bmax : 1u;
+// first B row of A group g and whether its triangle is needed
+__host__ __device__ __forceinline__ uint32_t g_blo(uint32_t s, uint32_t nc, uint32_t g, bool& tri) {
+    const uint32_t a0 = 32 * g, acnt = s - a0 < 32 ? s - a0 : 32u;
+    const bool full_core = a0 + acnt <= nc;
+    tri = !full_core && acnt >= 2;
+    const uint32_t b0 = a0 + acnt;
+    return full_core ? (nc > b0 ? nc : b0) : b0;
+}
+__host__ __device__ __forceinline__ uint32_t g_pieces(uint32_t s, uint32_t nc, uint32_t g, uint32_t bmax) {
+    bool tri;
+    const uint32_t blo = g_blo(s, nc, g, tri);
+    return s > blo ? (s - blo + bmax - 1) / bmax : (tri ? 1u : 0u);
 }
 __host__ __device__ __forceinline__ uint32_t big_groups(uint32_t s, uint32_t L) {
     return s <= 2 * L ? 1u : (s + 31) / 32;
 }
-__host__ __device__ __forceinline__ uint64_t big_items(uint32_t s, uint32_t L) {
+__host__ __device__ __forceinline__ uint64_t big_items(uint32_t s, uint32_t nc, uint32_t L) {
     if (s <= 2 * L) return 1;
     uint64_t c = 0;
-    for (uint32_t g = 0, ng = big_groups(s, L); g < ng; ++g) c += g_pieces(s, g, big_bmax(L));
+    for (uint32_t g = 0, ng = big_groups(s, L); g < ng; ++g) c += g_pieces(s, nc, g, big_bmax(L));
     return c;
 }
 
@@ -420,6 +435,38 @@ __device__ __forceinline__ void emit_chunks_tri(uint2* chunks, uint32_t base, ui
     }
 }
 
+// all chunks of a whole bucket of s rows whose first nc rows are core: per A
+// group the triangle (unless wholly core) and the B rows from g_blo
+__device__ __forceinline__ uint32_t chunks_nc(uint2* chunks, uint32_t s, uint32_t nc, uint32_t table,
+                                              bool fold, bool emit) {
+    uint32_t n = 0;
+    for (uint32_t c = 0; c * 32 < s; ++c) {
+        const uint32_t ab = c * 32, acnt = min(32u, s - ab);
+        bool tri;
+        const uint32_t blo = g_blo(s, nc, c, tri);
+        if (tri) {
+            if (fold) {
+                if (emit) chunks[n] = make_chunk(ab, acnt, 0, 0, true, table);
+                ++n;
+            } else {
+                const uint32_t np = n_pieces(ab + 1, ab + acnt);
+                for (uint32_t k = 0; k < np; ++k) {
+                    const uint32_t b0 = ab + 1 + k * BPIECE;
+                    if (emit) chunks[n] = make_chunk(ab, acnt, b0, min(ab + acnt, b0 + BPIECE), true, table);
+                    ++n;
+                }
+            }
+        }
+        const uint32_t np = n_pieces(blo, s);
+        for (uint32_t k = 0; k < np; ++k) {
+            const uint32_t b0 = blo + k * BPIECE;
+            if (emit) chunks[n] = make_chunk(ab, acnt, b0, min(s, b0 + BPIECE), false, table);
+            ++n;
+        }
+    }
+    return n;
+}
+
 template <int W, class Lay, int ROWP>
 __device__ __forceinline__ void stage_row(uint32_t* rows, uint32_t pos, const uint32_t* __restrict__ tags,
                                           uint64_t n, uint32_t id, uint32_t wg) {
@@ -443,6 +490,7 @@ struct Plan {
     const uint64_t* bigoff;      // exclusive prefix of items per big bucket
     const uint64_t* totals;      // [0] small members, [1] n_big, [2] n_tiles, [3] n_bigitems,
                                  // [4] max segments per bucket, [5] item table valid
+    const uint32_t* nc;          // core members per bucket, listed first (nullptr: none)
 };
 
 template <int W, int MODE, bool HAS_E, int WT, bool EX>
@@ -582,12 +630,12 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         else hi = mid;
                     }
                     bk = plan.bigb[lo];
-                    const uint32_t sb = bsize[bk];
+                    const uint32_t sb = bsize[bk], ncb = plan.nc ? plan.nc[bk] : 0u;
                     uint64_t rem = idx - plan.bigoff[lo];
                     uint32_t gg = 0;
                     if (sb > 2 * L) {
-                        while (rem >= g_pieces(sb, gg, big_bmax(L))) {
-                            rem -= g_pieces(sb, gg, big_bmax(L));
+                        while (rem >= g_pieces(sb, ncb, gg, big_bmax(L))) {
+                            rem -= g_pieces(sb, ncb, gg, big_bmax(L));
                             ++gg;
                         }
                     }
@@ -595,15 +643,17 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     J = (uint32_t)rem;
                 }
                 const uint32_t s = bsize[bk];
+                const uint32_t nc = plan.nc ? plan.nc[bk] : 0u;
                 const uint64_t st = bstart[bk];
                 uint32_t a0 = 0, nA = s, j0 = 0, nB = 0;  // s <= 2L: the whole bucket
+                bool gtri = true;
                 if (s > 2 * L) {
                     a0 = 32 * g;
                     nA = min(32u, s - a0);
-                    const uint32_t b0 = a0 + 32, lb = s > b0 ? s - b0 : 0;
+                    const uint32_t blo = g_blo(s, nc, g, gtri), lb = s > blo ? s - blo : 0;
                     if (lb) {
-                        const uint32_t np = g_pieces(s, g, big_bmax(L)), pl = (lb + np - 1) / np;
-                        j0 = b0 + J * pl;
+                        const uint32_t np = g_pieces(s, nc, g, big_bmax(L)), pl = (lb + np - 1) / np;
+                        j0 = blo + J * pl;
                         nB = min(pl, s - j0);
                     }
                 }
@@ -615,7 +665,10 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                 if (lane == 0) {
                     const uint32_t table = btab[bk];
                     uint32_t cbase = 0;
-                    if (J == 0) {  // the whole bucket, or group g's own triangle
+                    if (s <= 2 * L) {  // the whole bucket (pairs of two core rows left out)
+                        cbase = chunks_nc(chunks, s, nc, table, FOLD, true);
+                        nB = 0;
+                    } else if (J == 0 && gtri) {  // group g's own triangle
                         emit_chunks_tri(chunks, 0, 0, nA, table, FOLD);
                         cbase = count_chunks_tri(nA, FOLD);
                     }
@@ -770,7 +823,8 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     valid = a_ok && u >= (tri ? apos + 1 : bbeg);  // tri: pairs j > i
                     if (excl_on || HAS_E) {
                         const uint32_t bid = ids[u];
-                        if (excl_on) valid = valid && (uint64_t)(bid - a) > excl;  // ids ascend in a bucket
+                        // ids ascend in a bucket unless its list is core-first permuted
+                        if (excl_on) valid = valid && (uint64_t)(max(a, bid) - min(a, bid)) > excl;
                         if (HAS_E && valid && emask[bid] &&
                             (p <= 1 || part_of(edges, p, bid) == a_part))
                             valid = false;
@@ -841,7 +895,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     if (slow) {
                         const uint32_t e = (qhead + qn + __popc(bal & lt_mask)) & (QCAP - 1);
                         const uint32_t bid = ids[u];
-                        const uint32_t qa = fold ? min(a, bid) : a, qb = fold ? max(a, bid) : bid;
+                        const uint32_t qa = min(a, bid), qb = max(a, bid);
                         QS_DASSERT(e < QCAP && qa < qb && qb < n);
                         q.qa[e] = qa;
                         q.qb[e] = qb;
@@ -940,14 +994,14 @@ constexpr int SM_CLS = 2 + 3 * 34;  // u32 words of the class table (see k_small
 // tpre[34] at 68 (task prefix by size), cursor[34] at 102
 __global__ void k_small_count(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
                               uint32_t tmax, uint64_t nb, uint32_t smin, uint32_t smax,
-                              uint32_t* __restrict__ cls) {
+                              uint32_t* __restrict__ cls, const uint32_t* __restrict__ nc) {
     __shared__ uint32_t h[34];
     if (threadIdx.x < 34) h[threadIdx.x] = 0;
     __syncthreads();
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = bsize[i];
-        if (s >= smin && s <= smax && btab[i] <= tmax) atomicAdd(&h[s], 1u);
+        if (s >= smin && s <= smax && btab[i] <= tmax && !(nc && nc[i] >= s)) atomicAdd(&h[s], 1u);
     }
     __syncthreads();
     if (threadIdx.x < 34 && h[threadIdx.x]) atomicAdd(&cls[threadIdx.x], h[threadIdx.x]);
@@ -973,7 +1027,7 @@ constexpr int SM_SCAT = 4;  // buckets per thread
 __global__ void __launch_bounds__(256) k_small_scatter(
     const uint64_t* __restrict__ bstart, const uint32_t* __restrict__ bsize,
     const uint32_t* __restrict__ btab, uint32_t tmax, uint64_t nb, uint32_t smin, uint32_t smax,
-    uint32_t* __restrict__ cls, uint64_t* __restrict__ desc) {
+    uint32_t* __restrict__ cls, uint64_t* __restrict__ desc, const uint32_t* __restrict__ nc) {
     __shared__ uint32_t h[34], base[34];
     if (threadIdx.x < 34) h[threadIdx.x] = 0;
     __syncthreads();
@@ -985,7 +1039,7 @@ __global__ void __launch_bounds__(256) k_small_scatter(
         sz[k] = 0;
         if (i < nb) {
             const uint32_t s = bsize[i];
-            if (s >= smin && s <= smax && btab[i] <= tmax) {
+            if (s >= smin && s <= smax && btab[i] <= tmax && !(nc && nc[i] >= s)) {
                 sz[k] = s;
                 rk[k] = atomicAdd(&h[s], 1u);
             }
@@ -1229,11 +1283,12 @@ __global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) 
 __global__ void k_plan_sizes(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
                              uint32_t tmax, uint64_t nb, uint32_t L,
                              uint64_t* __restrict__ small, uint64_t* __restrict__ bigflag,
-                             uint32_t smin, uint32_t smax) {
+                             uint32_t smin, uint32_t smax, const uint32_t* __restrict__ nc) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = (i < nb && btab[i] <= tmax) ? bsize[i] : 0;
         if (s < smin || s > smax) s = 0;
+        if (nc && i < nb && nc[i] >= s) s = 0;  // wholly core: nothing left to compare
         small[i] = (i < nb && s <= L) ? s : 0;
         bigflag[i] = (i < nb && s > L) ? 1 : 0;
     }
@@ -1244,15 +1299,15 @@ __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* _
                            uint32_t tmax, uint64_t nb, uint32_t L,
                            const uint64_t* __restrict__ bigpos, uint64_t* __restrict__ bigb,
                            uint64_t* __restrict__ bigcnt, unsigned long long* __restrict__ maxnseg,
-                           uint32_t smin, uint32_t smax) {
+                           uint32_t smin, uint32_t smax, const uint32_t* __restrict__ nc) {
     uint32_t mx = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = bsize[i];
-        if (s <= L || btab[i] > tmax || s < smin || s > smax) continue;
+        const uint32_t s = bsize[i], ncb = nc ? nc[i] : 0u;
+        if (s <= L || btab[i] > tmax || s < smin || s > smax || ncb >= s) continue;
         const uint64_t k = bigpos[i];
         bigb[k] = i;
-        bigcnt[k] = big_items(s, L);
+        bigcnt[k] = big_items(s, ncb, L);
         mx = max(mx, big_groups(s, L));
     }
     // one atomic per warp (a single contended address otherwise serialises)
@@ -1263,16 +1318,17 @@ __global__ void k_plan_big(const uint32_t* __restrict__ bsize, const uint32_t* _
 
 __global__ void k_plan_bigitems(const uint32_t* __restrict__ bsize, const uint64_t* __restrict__ bigb,
                                 const uint64_t* __restrict__ bigoff, const uint64_t* __restrict__ totals,
-                                uint32_t L, uint64_t* __restrict__ items, uint64_t items_cap) {
+                                uint32_t L, uint64_t* __restrict__ items, uint64_t items_cap,
+                                const uint32_t* __restrict__ nc) {
     const uint64_t nbig = totals[1];
     if (totals[3] > items_cap || totals[4] > 4095) return;  // decoded on the fly instead
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nbig;
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = bigb[k];
-        const uint32_t sb = bsize[b], ng = big_groups(sb, L);
+        const uint32_t sb = bsize[b], ng = big_groups(sb, L), ncb = nc ? nc[b] : 0u;
         uint64_t o = bigoff[k];
         for (uint32_t g = 0; g < ng; ++g) {
-            const uint32_t np = sb > 2 * L ? g_pieces(sb, g, big_bmax(L)) : 1u;
+            const uint32_t np = sb > 2 * L ? g_pieces(sb, ncb, g, big_bmax(L)) : 1u;
             for (uint32_t J = 0; J < np; ++J) items[o++] = (b << 24) | ((uint64_t)g << 12) | J;
         }
     }
@@ -1399,7 +1455,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
                   uint64_t n, uint32_t t, uint32_t m, uint64_t excl, const uint8_t* emask,
                   const uint64_t* edges, uint32_t p, uint64_t* out_key, uint32_t* out_sim,
                   uint32_t* out_rest, uint64_t cap, unsigned long long* counters, uint64_t* ws,
-                  void* sws, void* smws, cudaStream_t st, uint32_t wg) {
+                  void* sws, void* smws, cudaStream_t st, uint32_t wg, const uint32_t* nc) {
     using C = TileCfg<W, MODE, WT>;
     const uint32_t L = C::L;
     uint64_t* mpre = ws;                       // nb + 1
@@ -1425,10 +1481,10 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
         smin = max(smin_env, SMALL_MAX + 1);
         if (lo <= hi) {
             QS_CUDA(cudaMemsetAsync(cls, 0, SM_CLS * 4, st), "memset");
-            k_small_count<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, lo, hi, cls);
+            k_small_count<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, lo, hi, cls, nc);
             k_small_prefix<<<1, 32, 0, st>>>(cls);
             k_small_scatter<<<(unsigned)((nb + 256 * SM_SCAT - 1) / (256 * SM_SCAT)), 256, 0, st>>>(
-                bstart, bsize, btab, tmax, nb, lo, hi, cls, desc);
+                bstart, bsize, btab, tmax, nb, lo, hi, cls, desc, nc);
             auto sk = excl > 0 ? k_pairs_small<W, MODE, HAS_E, WT, true>
                                : k_pairs_small<W, MODE, HAS_E, WT, false>;
             constexpr size_t ssm = 0;
@@ -1441,7 +1497,7 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
             QS_CHECK_LAUNCH("k_pairs_small");
         }
     }
-    k_plan_sizes<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, mpre, bigpos, smin, smax);
+    k_plan_sizes<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, mpre, bigpos, smin, smax, nc);
     int rc = scan_u64(mpre, mpre, nb + 1, totals + 0, sws, st);
     if (rc) return rc;
     rc = scan_u64(bigpos, bigpos, nb + 1, totals + 1, sws, st);
@@ -1449,14 +1505,14 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     QS_CUDA(cudaMemsetAsync(bigoff, 0, (nb + 1) * 8, st), "memset");
     QS_CUDA(cudaMemsetAsync(totals + 4, 0, 8, st), "memset");
     k_plan_big<<<g, 256, 0, st>>>(bsize, btab, tmax, nb, L, bigpos, bigb, bigoff,
-                                  (unsigned long long*)(totals + 4), smin, smax);
+                                  (unsigned long long*)(totals + 4), smin, smax, nc);
     rc = scan_u64(bigoff, bigoff, nb + 1, nullptr, sws, st);
     if (rc) return rc;
     k_plan_tiles<<<g, 256, 0, st>>>(mpre, nb, L, totals, bigoff, tile_first, items_cap);
-    k_plan_bigitems<<<g, 256, 0, st>>>(bsize, bigb, bigoff, totals, L, items, items_cap);
+    k_plan_bigitems<<<g, 256, 0, st>>>(bsize, bigb, bigoff, totals, L, items, items_cap, nc);
     QS_CUDA(cudaMemsetAsync(work, 0, 8, st), "memset");
     QS_CHECK_LAUNCH("plan");
-    Plan plan{mpre, tile_first, items, bigb, bigoff, totals};
+    Plan plan{mpre, tile_first, items, bigb, bigoff, totals, nc};
     auto kern = excl > 0 ? k_pairs_pc<W, MODE, HAS_E, WT, true> : k_pairs_pc<W, MODE, HAS_E, WT, false>;
     QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM),
             "smem attr");
@@ -1496,20 +1552,20 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
                           const uint8_t* emask, const uint64_t* edges, uint32_t p, uint64_t* ok,
                           uint32_t* os, uint32_t* orest, uint64_t cap,
                           unsigned long long* counters, uint64_t* ws, void* sws, void* smws,
-                          cudaStream_t st) {
+                          cudaStream_t st, uint32_t w_lo, uint32_t w_hi, const uint32_t* nc) {
     uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
     k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
     uint64_t hb[5] = {0, 0, 0, 0, 0};
     QS_CUDA(cudaMemcpyAsync(hb, dbounds, (W + 1) * 8, cudaMemcpyDeviceToHost, st), "copy");
     QS_CUDA(cudaStreamSynchronize(st), "sync");
-    for (uint32_t w = 0; w < W; ++w) {
+    for (uint32_t w = w_lo; w < W && w < w_hi; ++w) {
         const uint64_t a = hb[w], b = hb[w + 1];
         if (b <= a) continue;
         if (MODE == MODE_MATCHED && 32 * w > t - m) continue;  // no first collision there
 #define QS_W(WW, WTT)                                                                             \
     run_pc<WW, MODE, HAS_E, WTT>(sids, bstart + a, bsize + a, btab + a, b - a, rkeys, tags, n, t, \
                                  m, excl, emask, edges, p, ok, os, orest, cap, counters, ws, sws, \
-                                 smws, st, W)
+                                 smws, st, W, nc ? nc + a : nullptr)
         constexpr bool DI = MODE == MODE_DISTINCT;
         int rc = QS_OK;
         if (w == 0) {
@@ -1534,15 +1590,84 @@ static int dispatch_mode(int mode, bool has_e, const uint32_t* sids, const uint6
                          uint32_t m, uint64_t excl, const uint8_t* emask, const uint64_t* edges,
                          uint32_t p, uint64_t* ok, uint32_t* os, uint32_t* orest, uint64_t cap,
                          unsigned long long* counters, uint64_t* ws, void* sws, void* smws,
-                         cudaStream_t st) {
+                         cudaStream_t st, uint32_t w_lo, uint32_t w_hi, const uint32_t* nc) {
 #define QS_D(MM, EE) \
     run_word_split<W, MM, EE>(sids, bstart, bsize, btab, nb, rkeys, tags, n, t, m, excl, emask, \
-                              edges, p, ok, os, orest, cap, counters, ws, sws, smws, st)
+                              edges, p, ok, os, orest, cap, counters, ws, sws, smws, st, w_lo, \
+                              w_hi, nc)
     if (mode != MODE_MATCHED) orest = nullptr;  // lazy counts: MATCHED only
     if (mode == MODE_FULL) return has_e ? QS_D(MODE_FULL, true) : QS_D(MODE_FULL, false);
     if (mode == MODE_MATCHED) return has_e ? QS_D(MODE_MATCHED, true) : QS_D(MODE_MATCHED, false);
     return has_e ? QS_D(MODE_DISTINCT, true) : QS_D(MODE_DISTINCT, false);
 #undef QS_D
+}
+
+// Core-first member lists (buckets of tables >= table_lo): a stable partition of
+// each bucket's ids, the members flagged in `core` first, and their count.
+// Buckets of earlier tables get count 0 and are not copied.  A warp takes 32
+// consecutive buckets: a lane partitions its own bucket when it has <= 32
+// members (nearly all of them), the warp partitions the bigger ones together.
+__global__ void k_core_first(const uint32_t* __restrict__ sids, const uint64_t* __restrict__ bstart,
+                             const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                             uint64_t nb, uint32_t table_lo, const uint8_t* __restrict__ core,
+                             uint32_t* __restrict__ sids_out, uint32_t* __restrict__ nc) {
+    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t b0 = gw * 32; b0 < nb; b0 += nw * 32) {
+        const uint64_t b = b0 + lane;
+        bool mine = false, big = false;
+        uint32_t s = 0;
+        uint64_t st = 0;
+        if (b < nb) {
+            if (btab[b] < table_lo) {
+                nc[b] = 0;
+            } else {
+                s = bsize[b];
+                st = bstart[b];
+                mine = s <= 32;
+                big = !mine;
+            }
+        }
+        if (mine) {
+            uint32_t cm = 0;  // core bits of the members, in order
+            for (uint32_t i = 0; i < s; ++i) cm |= (core[sids[st + i]] ? 1u : 0u) << i;
+            const uint32_t ncore = __popc(cm);
+            uint32_t pc = 0, pn = ncore;
+            for (uint32_t i = 0; i < s; ++i) {
+                const uint32_t id = sids[st + i];
+                if ((cm >> i) & 1u) sids_out[st + pc++] = id;
+                else sids_out[st + pn++] = id;
+            }
+            nc[b] = ncore;
+        }
+        uint32_t bigm = __ballot_sync(0xffffffffu, big);
+        while (bigm) {
+            const uint32_t src = __ffs(bigm) - 1;
+            bigm &= bigm - 1;
+            const uint32_t sb = __shfl_sync(0xffffffffu, s, src);
+            const uint64_t sb0 = __shfl_sync(0xffffffffu, st, src);
+            uint32_t ncore = 0;
+            for (uint32_t i0 = 0; i0 < sb; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const bool c = i < sb && core[sids[sb0 + i]];
+                ncore += __popc(__ballot_sync(0xffffffffu, c));
+            }
+            uint32_t pc = 0, pn = ncore;
+            for (uint32_t i0 = 0; i0 < sb; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const uint32_t id = i < sb ? sids[sb0 + i] : 0u;
+                const bool c = i < sb && core[id];
+                const uint32_t bc = __ballot_sync(0xffffffffu, c);
+                const uint32_t bn = __ballot_sync(0xffffffffu, i < sb && !c);
+                if (c) sids_out[sb0 + pc + __popc(bc & lt)] = id;
+                else if (i < sb) sids_out[sb0 + pn + __popc(bn & lt)] = id;
+                pc += __popc(bc);
+                pn += __popc(bn);
+            }
+            if (lane == src) nc[b] = ncore;
+        }
+    }
 }
 
 // exact counts of lazily counted pairs: the candidate tables the drain left
@@ -1590,13 +1715,17 @@ size_t qs_lsh_pairs_ws_bytes(uint64_t n_nonsingle) {
            1024 + (size_t)(n_nonsingle + 1) * 8 + 64;
 }
 
-int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
-                 const uint32_t* btab_dev, uint64_t n_nonsingle, const uint64_t* rkeys_dev,
-                 const uint32_t* tags_dev, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
-                 const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
-                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev, uint64_t cap,
-                 unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes, void* stream) {
+int qs_lsh_pairs_ex(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
+                    const uint32_t* btab_dev, uint64_t n_nonsingle, const uint64_t* rkeys_dev,
+                    const uint32_t* tags_dev, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
+                    const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
+                    uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
+                    uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
+                    uint32_t word_lo, uint32_t word_hi, const uint32_t* core_count_dev,
+                    void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    QS_ARG(word_lo < word_hi, "empty table-word range");
+    QS_ARG(core_count_dev == nullptr || mode == 1, "core-first lists are for the matched pass");
     QS_ARG(ws_bytes >= qs_lsh_pairs_ws_bytes(n_nonsingle), "pairs workspace too small");
     QS_ARG(m >= 1 && m <= t, "min_matches must be in [1, tables]");
     QS_ARG(mode >= 0 && mode <= 2, "mode must be 0 (full), 1 (matched) or 2 (distinct)");
@@ -1610,13 +1739,16 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
 #define QS_D(WW)                                                                                  \
     dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, nb, rkeys_dev,      \
                       tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,           \
-                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, smws, st)
+                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, smws, st, word_lo,   \
+                      word_hi, core_count_dev)
     switch (W) {
         case 1: return QS_D(1);
         case 2: return QS_D(2);
         case 3: return QS_D(3);
         case 4: return QS_D(4);
         default: {
+            QS_ARG(word_lo == 0 && word_hi >= W && core_count_dev == nullptr,
+                   "table-word ranges and core-first lists need t <= 128");
             uint64_t* off = ws;
             k_chunk_counts<<<qs_blocks(nb + 1, 256), 256, 0, st>>>(bsize_dev, nb, off);
             int rc = scan_u64(off, off, nb + 1, nullptr, sws, st);
@@ -1630,6 +1762,31 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uin
         }
     }
 #undef QS_D
+}
+
+int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev, const uint32_t* bsize_dev,
+                 const uint32_t* btab_dev, uint64_t n_nonsingle, const uint64_t* rkeys_dev,
+                 const uint32_t* tags_dev, uint64_t n, uint32_t t, uint32_t m, uint64_t excl,
+                 const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
+                 uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev, uint64_t cap,
+                 unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes, void* stream) {
+    return qs_lsh_pairs_ex(sids_dev, bstart_dev, bsize_dev, btab_dev, n_nonsingle, rkeys_dev,
+                           tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, mode, out_key_dev,
+                           out_sim_dev, out_rest_dev, cap, counters_dev, ws_dev, ws_bytes, 0,
+                           0xFFFFFFFFu, nullptr, stream);
+}
+
+int qs_lsh_core_first(const uint32_t* sids_dev, const uint64_t* bstart_dev,
+                      const uint32_t* bsize_dev, const uint32_t* btab_dev, uint64_t n_nonsingle,
+                      uint32_t table_lo, const uint8_t* core_dev, uint32_t* sids_out_dev,
+                      uint32_t* core_count_dev, void* stream) {
+    if (n_nonsingle == 0) return QS_OK;
+    QS_ARG(core_dev != nullptr, "core mask required");
+    k_core_first<<<num_sms() * 16, 256, 0, (cudaStream_t)stream>>>(
+        sids_dev, bstart_dev, bsize_dev, btab_dev, n_nonsingle, table_lo, core_dev, sids_out_dev,
+        core_count_dev);
+    QS_CHECK_LAUNCH("k_core_first");
+    return QS_OK;
 }
 
 int qs_lsh_complete_sims(const uint64_t* pair_key_dev, uint32_t* pair_sim_dev,

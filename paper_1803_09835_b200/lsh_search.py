@@ -249,8 +249,13 @@ class DeviceSearch:
         self.compact_sizes = bsize2[:nb2]
         return (sids2, bstart2, bsize2, btab2, nb2)
 
-    def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None):
-        """Enumerate; returns (pair_key int64, pair_sim int32, n_matched, distinct)."""
+    def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None, word_range=None,
+              core_count=None):
+        """Enumerate; returns (pair_key int64, pair_sim int32, n_matched, distinct).
+
+        word_range: (lo, hi) restricts the pass to the buckets of table words
+        [lo, hi); core_count: per-bucket core counts of core-first `lists`
+        (qs_lsh_pairs_ex: pairs of two core members are skipped)."""
         torch, lib = self.torch, nat.lib()
         sids, bstart, bsize, btab, nb = lists if lists is not None else self.full
         self._mark(("pairs_full", "pairs_matched", "pairs_distinct")[mode])
@@ -268,11 +273,19 @@ class DeviceSearch:
             ps = torch.empty(max(cap, 1), dtype=torch.int32, device=self.dev)
             rest = torch.empty(max(cap, 1) * W, dtype=torch.int32, device=self.dev) if lazy else None
             counters.zero_()
-            nat.call("qs_lsh_pairs", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize), nat.ptr(btab),
-                     nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n, self.t, m, excl,
-                     nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk), nat.ptr(ps),
-                     nat.ptr(rest), cap, nat.ptr(counters), nat.ptr(ws), ws.numel(),
-                     nat.stream())
+            if word_range is None and core_count is None:
+                nat.call("qs_lsh_pairs", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize),
+                         nat.ptr(btab), nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n,
+                         self.t, m, excl, nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk),
+                         nat.ptr(ps), nat.ptr(rest), cap, nat.ptr(counters), nat.ptr(ws),
+                         ws.numel(), nat.stream())
+            else:
+                lo, hi = word_range if word_range is not None else (0, 0xFFFFFFFF)
+                nat.call("qs_lsh_pairs_ex", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize),
+                         nat.ptr(btab), nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n,
+                         self.t, m, excl, nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk),
+                         nat.ptr(ps), nat.ptr(rest), cap, nat.ptr(counters), nat.ptr(ws),
+                         ws.numel(), lo, hi, nat.ptr(core_count), nat.stream())
             # word bounds + per launched table word: 7 planning kernels, 2x3 scan kernels, pairs
             words = (self.t + 31) // 32
             if mode == self.MODE_MATCHED:
@@ -289,6 +302,46 @@ class DeviceSearch:
         if lazy:
             self._lazy = (pk, rest[: matched * W])
         return pk, ps, matched, distinct
+
+    def core_first(self, core, table_lo):
+        """Core-first copies of the member lists of tables >= table_lo and the
+        per-bucket core counts (qs_lsh_core_first)."""
+        torch = self.torch
+        sids2 = torch.empty_like(self.sids)
+        nc = torch.empty(max(self.nb, 1), dtype=torch.int32, device=self.dev)
+        nat.call("qs_lsh_core_first", nat.ptr(self.sids), nat.ptr(self.bstart), nat.ptr(self.bsize),
+                 nat.ptr(self.btab), self.nb, table_lo, nat.ptr(core), nat.ptr(sids2), nat.ptr(nc),
+                 nat.stream())
+        self.launches += 1
+        return (sids2, self.bstart, self.bsize, self.btab, self.nb), nc
+
+    def matched_core_skip(self, m, excl, edges, threshold):
+        """Pass 1 of the occurrence filter (partitions == 1) in two steps: the
+        buckets of the first table word as usual; then, with the fingerprints
+        whose degree over those pairs already exceeds the limit marked core, the
+        later words over core-first lists with pairs of two core members
+        skipped.  A partial degree is a lower bound of the full one, so those
+        fingerprints are core in the full count too; a skipped pair only joins
+        two excluded fingerprints and changes no degree decision, exclusion or
+        emitted triplet (lsh_search.py:256-287).  Returns what pairs() returns
+        for the whole MATCHED pass (the pair list is a different but equally
+        sufficient set: the same core set, exclusions and surviving pairs)."""
+        torch = self.torch
+        W = (self.t + 31) // 32
+        pk0, ps0, m0, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, word_range=(0, 1))
+        lz0 = self._lazy[1] if getattr(self, "_lazy", None) is not None else None
+        deg = self.occ_degree(pk0, m0, edges, 1)
+        core = (deg.to(torch.float64) > float(threshold) * self.n).to(torch.uint8)
+        lists, nc = self.core_first(core, 32)
+        pk1, ps1, m1, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, lists=lists,
+                                     word_range=(1, W), core_count=nc)
+        lz1 = self._lazy[1] if getattr(self, "_lazy", None) is not None else None
+        del lists, nc
+        pk = torch.cat([pk0, pk1])
+        ps = torch.cat([ps0, ps1])
+        if lz0 is not None and lz1 is not None:
+            self._lazy = (pk, torch.cat([lz0, lz1]))
+        return pk, ps, m0 + m1, 0
 
     def complete_sims(self, pk, ps, matched):
         """Exact sims for lazily counted MATCHED pairs (the tables left
@@ -436,8 +489,13 @@ def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_w
     if cfg.occurrence_threshold is None:
         pk, ps, matched, distinct = ds.pairs(ds.MODE_FULL, m, excl, None, edges, p)
     else:
-        # pass 1: matched pairs (no exclusions yet) -> occurrence filter
-        pk, ps, matched, _ = ds.pairs(ds.MODE_MATCHED, m, excl, None, edges, p)
+        # pass 1: matched pairs (no exclusions yet) -> occurrence filter; with one
+        # partition and t in (32, 128] the later table words skip pairs of two
+        # fingerprints the first word already proves core (QS_CORE_SKIP=0: off)
+        if p == 1 and 32 < t <= 128 and os.environ.get("QS_CORE_SKIP", "1") != "0":
+            pk, ps, matched, _ = ds.matched_core_skip(m, excl, edges, cfg.occurrence_threshold)
+        else:
+            pk, ps, matched, _ = ds.pairs(ds.MODE_MATCHED, m, excl, None, edges, p)
         emask, n_ex = ds.occurrence(pk, ps, matched, cfg.occurrence_threshold, edges, p)
         if n_ex == 0:
             emask = None
