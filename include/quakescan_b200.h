@@ -206,8 +206,8 @@ int qs_lsh_pairs(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                  uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
                  void* stream);
 
-/* qs_lsh_pairs restricted to the buckets of table words [word_lo, word_hi)
- * (table word = table / 32; t <= 128).  core_count_dev (mode 1 only, may be
+/* qs_lsh_pairs restricted to the buckets of tables [table_lo, table_hi)
+ * (t <= 128; the first-table rule still looks at every earlier table).  core_count_dev (mode 1 only, may be
  * NULL): the member lists are core-first (qs_lsh_core_first) and bucket b's
  * first core_count_dev[b] members are fingerprints already known to exceed
  * the occurrence limit; pairs of two of them are skipped — they change no
@@ -220,7 +220,7 @@ int qs_lsh_pairs_ex(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                     const uint64_t* edges_dev, uint32_t p, int mode,
                     uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
                     uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
-                    uint32_t word_lo, uint32_t word_hi, const uint32_t* core_count_dev,
+                    uint32_t table_lo, uint32_t table_hi, const uint32_t* core_count_dev,
                     void* stream);
 
 /* Core-first member lists for qs_lsh_pairs_ex: for every bucket of a table

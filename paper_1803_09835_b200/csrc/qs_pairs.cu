@@ -1527,13 +1527,14 @@ static int run_pc(const uint32_t* sids, const uint64_t* bstart, const uint32_t* 
     return QS_OK;
 }
 
-// first bucket of each table word (btab is non-decreasing): bounds[w] for w <= W
+// first bucket of each table word (btab is non-decreasing): bounds[w] for w <= W,
+// then the first buckets of tables table_lo and table_hi (bounds[W + 1], [W + 2])
 __global__ void k_word_bounds(const uint32_t* __restrict__ btab, uint64_t nb, uint32_t W,
-                              uint64_t* __restrict__ bounds) {
+                              uint32_t table_lo, uint32_t table_hi, uint64_t* __restrict__ bounds) {
     const uint32_t w = threadIdx.x;
-    if (w > W) return;
+    if (w > W + 2) return;
     uint64_t lo = 0, hi = nb;
-    const uint32_t target = w * 32;
+    const uint32_t target = w <= W ? w * 32 : (w == W + 1 ? table_lo : table_hi);
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
         if (btab[mid] < target) lo = mid + 1;
@@ -1552,14 +1553,15 @@ static int run_word_split(const uint32_t* sids, const uint64_t* bstart, const ui
                           const uint8_t* emask, const uint64_t* edges, uint32_t p, uint64_t* ok,
                           uint32_t* os, uint32_t* orest, uint64_t cap,
                           unsigned long long* counters, uint64_t* ws, void* sws, void* smws,
-                          cudaStream_t st, uint32_t w_lo, uint32_t w_hi, const uint32_t* nc) {
+                          cudaStream_t st, uint32_t t_lo, uint32_t t_hi, const uint32_t* nc) {
     uint64_t* dbounds = ws + (nb + 1) * 13;  // 8 spare words after the plan arrays
-    k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, dbounds);
-    uint64_t hb[5] = {0, 0, 0, 0, 0};
-    QS_CUDA(cudaMemcpyAsync(hb, dbounds, (W + 1) * 8, cudaMemcpyDeviceToHost, st), "copy");
+    k_word_bounds<<<1, 32, 0, st>>>(btab, nb, W, t_lo, t_hi, dbounds);
+    uint64_t hb[7] = {0, 0, 0, 0, 0, 0, 0};
+    QS_CUDA(cudaMemcpyAsync(hb, dbounds, (W + 3) * 8, cudaMemcpyDeviceToHost, st), "copy");
     QS_CUDA(cudaStreamSynchronize(st), "sync");
-    for (uint32_t w = w_lo; w < W && w < w_hi; ++w) {
-        const uint64_t a = hb[w], b = hb[w + 1];
+    const uint64_t ta = hb[W + 1], tb = t_hi >= t ? nb : hb[W + 2];  // buckets of [t_lo, t_hi)
+    for (uint32_t w = 0; w < W; ++w) {
+        const uint64_t a = max(hb[w], ta), b = min(hb[w + 1], tb);
         if (b <= a) continue;
         if (MODE == MODE_MATCHED && 32 * w > t - m) continue;  // no first collision there
 #define QS_W(WW, WTT)                                                                             \
@@ -1721,10 +1723,10 @@ int qs_lsh_pairs_ex(const uint32_t* sids_dev, const uint64_t* bstart_dev, const 
                     const uint8_t* excluded_dev, const uint64_t* edges_dev, uint32_t p, int mode,
                     uint64_t* out_key_dev, uint32_t* out_sim_dev, uint32_t* out_rest_dev,
                     uint64_t cap, unsigned long long* counters_dev, void* ws_dev, size_t ws_bytes,
-                    uint32_t word_lo, uint32_t word_hi, const uint32_t* core_count_dev,
+                    uint32_t table_lo, uint32_t table_hi, const uint32_t* core_count_dev,
                     void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    QS_ARG(word_lo < word_hi, "empty table-word range");
+    QS_ARG(table_lo < table_hi, "empty table range");
     QS_ARG(core_count_dev == nullptr || mode == 1, "core-first lists are for the matched pass");
     QS_ARG(ws_bytes >= qs_lsh_pairs_ws_bytes(n_nonsingle), "pairs workspace too small");
     QS_ARG(m >= 1 && m <= t, "min_matches must be in [1, tables]");
@@ -1739,16 +1741,16 @@ int qs_lsh_pairs_ex(const uint32_t* sids_dev, const uint64_t* bstart_dev, const 
 #define QS_D(WW)                                                                                  \
     dispatch_mode<WW>(mode, has_e, sids_dev, bstart_dev, bsize_dev, btab_dev, nb, rkeys_dev,      \
                       tags_dev, n, t, m, excl, excluded_dev, edges_dev, p, out_key_dev,           \
-                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, smws, st, word_lo,   \
-                      word_hi, core_count_dev)
+                      out_sim_dev, out_rest_dev, cap, counters_dev, ws, sws, smws, st, table_lo,  \
+                      table_hi, core_count_dev)
     switch (W) {
         case 1: return QS_D(1);
         case 2: return QS_D(2);
         case 3: return QS_D(3);
         case 4: return QS_D(4);
         default: {
-            QS_ARG(word_lo == 0 && word_hi >= W && core_count_dev == nullptr,
-                   "table-word ranges and core-first lists need t <= 128");
+            QS_ARG(table_lo == 0 && table_hi >= t && core_count_dev == nullptr,
+                   "table ranges and core-first lists need t <= 128");
             uint64_t* off = ws;
             k_chunk_counts<<<qs_blocks(nb + 1, 256), 256, 0, st>>>(bsize_dev, nb, off);
             int rc = scan_u64(off, off, nb + 1, nullptr, sws, st);

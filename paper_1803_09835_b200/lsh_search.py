@@ -31,6 +31,12 @@ PROFILES = {"baseline": (6, 5), "optimized": (8, 2)}
 _HIST_LEN = 1 << 16
 # MATCHED pass counts lazily (exact sims completed for filter survivors only)
 _LAZY_COUNTS = os.environ.get("QS_LAZY_COUNTS", "1") != "0"
+# occurrence-filtered MATCHED pass: tables [0, _CORE_SPLIT) first, then the rest
+# with pairs of two already-core fingerprints skipped (matched_core_skip).  At
+# cfg1 the first 32 tables prove the noise-group members core (MATCHED 218 ->
+# 189 ms); splits of 4-16 tables prove too few of them and only add launches
+# (220-199 ms, tools/gpu_r02at.sh)
+_CORE_SPLIT = int(os.environ.get("QS_CORE_SPLIT", "32"))
 _cap_hint = {}
 
 
@@ -249,11 +255,11 @@ class DeviceSearch:
         self.compact_sizes = bsize2[:nb2]
         return (sids2, bstart2, bsize2, btab2, nb2)
 
-    def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None, word_range=None,
+    def pairs(self, mode, m, excl, emask, edges, p, lists=None, cap=None, table_range=None,
               core_count=None):
         """Enumerate; returns (pair_key int64, pair_sim int32, n_matched, distinct).
 
-        word_range: (lo, hi) restricts the pass to the buckets of table words
+        table_range: (lo, hi) restricts the pass to the buckets of tables
         [lo, hi); core_count: per-bucket core counts of core-first `lists`
         (qs_lsh_pairs_ex: pairs of two core members are skipped)."""
         torch, lib = self.torch, nat.lib()
@@ -273,14 +279,14 @@ class DeviceSearch:
             ps = torch.empty(max(cap, 1), dtype=torch.int32, device=self.dev)
             rest = torch.empty(max(cap, 1) * W, dtype=torch.int32, device=self.dev) if lazy else None
             counters.zero_()
-            if word_range is None and core_count is None:
+            if table_range is None and core_count is None:
                 nat.call("qs_lsh_pairs", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize),
                          nat.ptr(btab), nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n,
                          self.t, m, excl, nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk),
                          nat.ptr(ps), nat.ptr(rest), cap, nat.ptr(counters), nat.ptr(ws),
                          ws.numel(), nat.stream())
             else:
-                lo, hi = word_range if word_range is not None else (0, 0xFFFFFFFF)
+                lo, hi = table_range if table_range is not None else (0, 0xFFFFFFFF)
                 nat.call("qs_lsh_pairs_ex", nat.ptr(sids), nat.ptr(bstart), nat.ptr(bsize),
                          nat.ptr(btab), nb, nat.ptr(self.rkeys), nat.ptr(self.tags), self.n,
                          self.t, m, excl, nat.ptr(emask), nat.ptr(edges), p, mode, nat.ptr(pk),
@@ -317,9 +323,9 @@ class DeviceSearch:
 
     def matched_core_skip(self, m, excl, edges, threshold):
         """Pass 1 of the occurrence filter (partitions == 1) in two steps: the
-        buckets of the first table word as usual; then, with the fingerprints
+        buckets of the first _CORE_SPLIT tables as usual; then, with the fingerprints
         whose degree over those pairs already exceeds the limit marked core, the
-        later words over core-first lists with pairs of two core members
+        later tables over core-first lists with pairs of two core members
         skipped.  A partial degree is a lower bound of the full one, so those
         fingerprints are core in the full count too; a skipped pair only joins
         two excluded fingerprints and changes no degree decision, exclusion or
@@ -327,14 +333,14 @@ class DeviceSearch:
         for the whole MATCHED pass (the pair list is a different but equally
         sufficient set: the same core set, exclusions and surviving pairs)."""
         torch = self.torch
-        W = (self.t + 31) // 32
-        pk0, ps0, m0, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, word_range=(0, 1))
+        t1 = min(self.t, _CORE_SPLIT)
+        pk0, ps0, m0, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, table_range=(0, t1))
         lz0 = self._lazy[1] if getattr(self, "_lazy", None) is not None else None
         deg = self.occ_degree(pk0, m0, edges, 1)
         core = (deg.to(torch.float64) > float(threshold) * self.n).to(torch.uint8)
-        lists, nc = self.core_first(core, 32)
+        lists, nc = self.core_first(core, t1)
         pk1, ps1, m1, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, lists=lists,
-                                     word_range=(1, W), core_count=nc)
+                                     table_range=(t1, self.t), core_count=nc)
         lz1 = self._lazy[1] if getattr(self, "_lazy", None) is not None else None
         del lists, nc
         pk = torch.cat([pk0, pk1])
@@ -490,9 +496,9 @@ def run_search(keys, rkeys, tags, n: int, t: int, cfg: SearchConfig, exclusion_w
         pk, ps, matched, distinct = ds.pairs(ds.MODE_FULL, m, excl, None, edges, p)
     else:
         # pass 1: matched pairs (no exclusions yet) -> occurrence filter; with one
-        # partition and t in (32, 128] the later table words skip pairs of two
-        # fingerprints the first word already proves core (QS_CORE_SKIP=0: off)
-        if p == 1 and 32 < t <= 128 and os.environ.get("QS_CORE_SKIP", "1") != "0":
+        # partition and _CORE_SPLIT < t <= 128 the later tables skip pairs of two
+        # fingerprints the first tables already prove core (QS_CORE_SKIP=0: off)
+        if p == 1 and _CORE_SPLIT < t <= 128 and os.environ.get("QS_CORE_SKIP", "1") != "0":
             pk, ps, matched, _ = ds.matched_core_skip(m, excl, edges, cfg.occurrence_threshold)
         else:
             pk, ps, matched, _ = ds.pairs(ds.MODE_MATCHED, m, excl, None, edges, p)
