@@ -232,6 +232,13 @@ int qs_lsh_core_first(const uint32_t* sids_dev, const uint64_t* bstart_dev,
                       uint32_t table_lo, const uint8_t* core_dev, uint32_t* sids_out_dev,
                       uint32_t* core_count_dev, void* stream);
 
+/* Number of core-core pairs qs_lsh_pairs_ex (mode 1, core-first lists of
+ * tables >= table_lo) leaves out, added to *out_dev (measurement: the pairs
+ * the pass compares = all pairs of its buckets minus these). */
+int qs_lsh_core_skipped(const uint32_t* bsize_dev, const uint32_t* btab_dev,
+                        const uint32_t* core_count_dev, uint64_t n_nonsingle, uint32_t t,
+                        uint32_t m, uint32_t table_lo, unsigned long long* out_dev, void* stream);
+
 /* Exact counts of lazily counted pairs (see qs_lsh_pairs): pair_sim_dev[i] +=
  * the agreeing tables among rest_dev[i * ceil(t/32) ...]. */
 int qs_lsh_complete_sims(const uint64_t* pair_key_dev, uint32_t* pair_sim_dev,

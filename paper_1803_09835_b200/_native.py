@@ -78,6 +78,7 @@ SIGNATURES = {
     "qs_lsh_pairs_ex": (_int, [_p, _p, _p, _p, _u64, _p, _p, _u64, _u32, _u32, _u64, _p, _p, _u32,
                                _int, _p, _p, _p, _u64, _p, _p, _sz, _u32, _u32, _p, _p]),
     "qs_lsh_core_first": (_int, [_p, _p, _p, _p, _u64, _u32, _p, _p, _p, _p]),
+    "qs_lsh_core_skipped": (_int, [_p, _p, _p, _u64, _u32, _u32, _u32, _p, _p]),
     "qs_lsh_complete_sims": (_int, [_p, _p, _p, _u64, _p, _u32, _p]),
     "qs_lsh_occurrence_filter": (_int, [_p, _p, _u64, _u64, _dbl, _p, _u32, _p, _p, _p, _p]),
     "qs_lsh_occ_degree": (_int, [_p, _u64, _p, _u32, _p, _p]),

@@ -1672,6 +1672,30 @@ __global__ void k_core_first(const uint32_t* __restrict__ sids, const uint64_t* 
     }
 }
 
+// Pairs of two core members the MATCHED pass over core-first lists leaves out
+// (the planning rules of k_plan_sizes / g_blo / chunks_nc and the small-bucket
+// planning): a wholly core bucket entirely; in a bucket of more than L members
+// every pair (i, j), i < j < nc, whose row i lies in a wholly core A group.
+__global__ void k_core_skipped(const uint32_t* __restrict__ bsize, const uint32_t* __restrict__ btab,
+                               const uint32_t* __restrict__ nc, uint64_t nb, uint32_t table_lo,
+                               uint32_t tmax, uint32_t L, unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t tb = btab[i];
+        if (tb < table_lo || tb > tmax) continue;
+        const uint64_t sz = bsize[i], c = nc[i];
+        if (c >= sz) acc += sz * (sz - 1) / 2;
+        else if (sz > L) {
+            const uint64_t f = 32 * (c / 32);
+            acc += f * (f - 1) / 2 + f * (c - f);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 // exact counts of lazily counted pairs: the candidate tables the drain left
 // unexamined (rest, W words per pair) are confirmed on the keys now
 __global__ void k_complete_sims(const uint64_t* __restrict__ pk, uint32_t* __restrict__ ps,
@@ -1788,6 +1812,21 @@ int qs_lsh_core_first(const uint32_t* sids_dev, const uint64_t* bstart_dev,
         sids_dev, bstart_dev, bsize_dev, btab_dev, n_nonsingle, table_lo, core_dev, sids_out_dev,
         core_count_dev);
     QS_CHECK_LAUNCH("k_core_first");
+    return QS_OK;
+}
+
+int qs_lsh_core_skipped(const uint32_t* bsize_dev, const uint32_t* btab_dev,
+                        const uint32_t* core_count_dev, uint64_t n_nonsingle, uint32_t t,
+                        uint32_t m, uint32_t table_lo, unsigned long long* out_dev, void* stream) {
+    if (n_nonsingle == 0) return QS_OK;
+    QS_ARG(t >= 1 && t <= 128 && m >= 1 && m <= t, "bad t / m");
+    const uint32_t W = (t + 31) >> 5;
+    const uint32_t L = W == 1 ? TileCfg<1, MODE_MATCHED, 0>::L
+                     : W == 2 ? TileCfg<2, MODE_MATCHED, 0>::L
+                     : W == 3 ? TileCfg<3, MODE_MATCHED, 0>::L : TileCfg<4, MODE_MATCHED, 0>::L;
+    k_core_skipped<<<qs_blocks(n_nonsingle, 256), 256, 0, (cudaStream_t)stream>>>(
+        bsize_dev, btab_dev, core_count_dev, n_nonsingle, table_lo, t - m, L, out_dev);
+    QS_CHECK_LAUNCH("k_core_skipped");
     return QS_OK;
 }
 

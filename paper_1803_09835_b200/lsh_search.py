@@ -342,6 +342,11 @@ class DeviceSearch:
         pk1, ps1, m1, _ = self.pairs(self.MODE_MATCHED, m, excl, None, edges, 1, lists=lists,
                                      table_range=(t1, self.t), core_count=nc)
         lz1 = self._lazy[1] if getattr(self, "_lazy", None) is not None else None
+        if self.timing:  # measurement: core-core pairs left out (bench.py roofline)
+            sk = torch.zeros(1, dtype=torch.int64, device=self.dev)
+            nat.call("qs_lsh_core_skipped", nat.ptr(self.bsize), nat.ptr(self.btab), nat.ptr(nc),
+                     self.nb, self.t, m, t1, nat.ptr(sk), nat.stream())
+            self.core_skipped = sk
         del lists, nc
         pk = torch.cat([pk0, pk1])
         ps = torch.cat([ps0, ps1])
