@@ -231,7 +231,8 @@ class _Chain:
     """Device state of one channel: samples, band spectrogram and the
     window-kernel tables (geometry of fingerprint.py:198-243)."""
 
-    def __init__(self, ts, params: FingerprintParams, full_band: bool = False):
+    def __init__(self, ts, params: FingerprintParams, full_band: bool = False,
+                 windows: bool = False):
         params.validate()
         self.torch = torch = nat.torch()
         self.params = params
@@ -251,6 +252,11 @@ class _Chain:
         tw = np.stack([taper * np.cos(ang), -taper * np.sin(ang)], axis=-1)
         self.tw = torch.from_numpy(np.ascontiguousarray(tw)).cuda()
         self.band = torch.empty((max(self.n_cols, 1), self.nb), dtype=torch.float32, device="cuda")
+        if windows:
+            # the window tables go up before the STFT launch: their pageable
+            # H2D copies would otherwise wait for it, and the host work that
+            # follows (the MAD sample draw) would no longer overlap it
+            self.prepare_windows()
         x = ts.samples
         n_samples = ts.n_samples
         frame, hop, nb = self.frame, self.hop, self.nb
@@ -443,8 +449,7 @@ def estimate_mad(ts, params: FingerprintParams, rate: float = 0.1, seed: int = 0
     total = n_windows(ts, params)
     if total == 0:
         raise DataError("series shorter than one fingerprint window")
-    ch = _Chain(ts, params)
-    ch.prepare_windows()
+    ch = _Chain(ts, params, windows=True)
     med, mad, n_sample = _mad_from_chain(ch, params, rate, seed, total)
     return MadStats(median=med.cpu().numpy(), mad=mad.cpu().numpy(), rate=float(rate),
                     seed=int(seed), n_sampled=int(n_sample), n_total=int(total))
@@ -497,6 +502,13 @@ def topk_bits(coeffs, stats: MadStats, top_k: int) -> np.ndarray:
     return out.cpu().numpy().view(np.uint32)
 
 
+def _index_columns(ts, params, total):
+    # window index and start epoch per fingerprint (fingerprint.py:612-613)
+    indices = np.arange(total, dtype=np.uint64)
+    epochs = ts.start_epoch_s + np.arange(total) * params.window_lag_s
+    return indices, epochs
+
+
 def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = None,
                        mad_rate: float = 0.1, mad_seed: int = 0,
                        batch: int = 512) -> tuple[FingerprintSet, MadStats]:
@@ -507,10 +519,9 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
     params.validate()
     torch = nat.torch()
     total = n_windows(ts, params)
-    ch = _Chain(ts, params)
     if total == 0:
         raise DataError("series shorter than one fingerprint window")
-    ch.prepare_windows()
+    ch = _Chain(ts, params, windows=True)
     if stats is None:
         if not 0 < mad_rate <= 1:
             raise ParameterError(f"sampling rate must be in (0, 1], got {mad_rate}")
@@ -526,8 +537,10 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
     if params.top_k > n_eligible:
         raise ParameterError(f"top_k={params.top_k} exceeds {n_eligible} coefficients with nonzero MAD")
     bits = torch.empty((total, params.top_k), dtype=torch.int32, device="cuda")
+    # the host-side index/epoch columns are filled while the main pass runs
     if nat.is_device_tensor(ts.samples):
         ch.windows(3, bits, win0=0, n=total, med=med, mad=mad, top_k=params.top_k)
+        indices, epochs = _index_columns(ts, params, total)
         ch.check_finite()
         out_bits = bits
     else:
@@ -548,11 +561,10 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
             with torch.cuda.stream(copy):
                 host[c0:c1].copy_(bits[c0:c1], non_blocking=True)
         bits.record_stream(copy)
+        indices, epochs = _index_columns(ts, params, total)
         copy.synchronize()
         ch.check_finite()
         out_bits = host.numpy().view(np.uint32)
-    indices = np.arange(total, dtype=np.uint64)
-    epochs = ts.start_epoch_s + np.arange(total) * params.window_lag_s
     fps = FingerprintSet(d=params.d, top_k=params.top_k, window_len_s=params.window_len_s,
                          window_lag_s=params.window_lag_s, indices=indices, epochs=epochs,
                          bits=out_bits,

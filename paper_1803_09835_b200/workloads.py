@@ -278,3 +278,44 @@ def cfg3_trace_torch(n_samples=3_150_000_000, seed=3, repeats=2000, periodic=50,
             src[0, s0:s0 + L] = wd
             view.index_add_(0, rows, src.expand(rows.numel(), cell))
     return x, {"events": ev_truth, "periodic": periodic, "cells": cells}
+
+
+def cfg4_events(n_samples=3_150_000_000, seed=4, repeats=2000, stations=10, max_delay_s=8.0,
+                gain=(0.3, 3.0)):
+    """cfg4's shared event catalogue: `repeats` planted copies of the cfg0
+    chirp templates at uniform times (amplitude log-uniform 0.2..2 x RMS at a
+    unit-gain station), each arriving at every station with its own delay
+    U(0, max_delay_s), and one gain per station, log-uniform in `gain`."""
+    rng = np.random.default_rng(seed)
+    events = chirp_templates(rng)
+    per = max(1, repeats // len(events))
+    L = events[0].size
+    span = n_samples - L - int(max_delay_s * SR_HZ) - 1
+    cat = []
+    for ti in range(len(events)):
+        offs = rng.integers(0, span, size=per)
+        amps = 10.0 ** rng.uniform(math.log10(0.2), math.log10(2.0), size=per)
+        cat.extend((ti, int(o), float(a)) for o, a in zip(offs, amps))
+    delays = np.round(rng.uniform(0.0, max_delay_s, size=(stations, len(cat))) * SR_HZ).astype(np.int64)
+    gains = 10.0 ** rng.uniform(math.log10(gain[0]), math.log10(gain[1]), size=stations)
+    return {"templates": events, "catalogue": cat, "delays": delays, "gains": gains}
+
+
+def cfg4_station_torch(station, ev, n_samples=3_150_000_000, seed=4, device="cuda",
+                       chunk=1 << 26):
+    """cfg4 (10 stations x 1 year at 100 Hz) on the GPU, one station at a
+    time: independent seeded N(0, 1) float32 noise per station plus the shared
+    catalogue of `cfg4_events`, delayed and scaled per station."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1000 + station)
+    x = torch.empty(n_samples, dtype=torch.float32, device=device)
+    for a in range(0, n_samples, chunk):
+        b = min(n_samples, a + chunk)
+        x[a:b] = torch.randn(b - a, generator=g, device=device, dtype=torch.float32)
+    wds = [torch.from_numpy(w).to(device) for w in ev["templates"]]
+    gain = float(ev["gains"][station])
+    for (ti, o, amp), dl in zip(ev["catalogue"], ev["delays"][station]):
+        s0 = o + int(dl)
+        x[s0:s0 + wds[ti].numel()] += gain * amp * wds[ti]
+    return x
