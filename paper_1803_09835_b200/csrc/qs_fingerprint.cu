@@ -82,6 +82,94 @@ __global__ void __launch_bounds__(STFT_COLS) k_band_stft(const TX* __restrict__ 
     }
 }
 
+// ------------------------------------------------- STFT on the FP64 tensor cores
+// The band DFT is a dense contraction: out[c][n] = sum_j X[c][j] B[j][n] with
+// X[c][j] = x[c hop + j] (a Toeplitz view of the trace, K = frame) and
+// B[j][2b + r] the tapered twiddles of band bin b (r = 0: cos, 1: -sin).  One
+// warp computes SM_MT m-tiles of 8 columns against 4 n-tiles of 8 outputs per
+// k-step of 4 samples with DMMA (mma.sync m8n8k4 f64: A row = lane / 4,
+// k = lane % 4; B k = lane % 4, n = lane / 4; C row = lane / 4, n = 2 (lane %
+// 4) + {0, 1}, i.e. each lane ends with the (re, im) pair of one bin of one
+// column).  B is staged once per CTA in fragment order (conflict-free 8-byte
+// loads), the samples per 256-column slab as f64.  Padded k (frame % 4) reads
+// zero samples; padded n reads zero twiddles.  Summation order differs from
+// the FMA chain only at f64 rounding level; power, log10 and the f32 store
+// are the same as k_band_stft.
+constexpr int SM_WARPS = 8, SM_MT = 4;
+constexpr int SM_COLS = SM_WARPS * SM_MT * 8;  // 256 columns per slab
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(SM_WARPS * 32, 2) k_band_stft_mma(
+    const TX* __restrict__ x, uint64_t n_samples, uint32_t frame, uint32_t hop, uint64_t n_cols,
+    uint32_t nb, const double* __restrict__ tw, float* __restrict__ out, uint32_t b_first,
+    uint32_t ld_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t ksteps = (frame + 3) / 4;
+    const uint32_t ntiles = (2 * nb + 7) / 8;            // n-tiles of 8 outputs
+    const uint32_t ngroups = (ntiles + 3) / 4;           // 4 n-tiles per pass
+    double* bs = (double*)smem;                           // [ksteps][ngroups * 4][32]
+    const uint32_t nt_pad = ngroups * 4;
+    double* xs = bs + (uint64_t)ksteps * nt_pad * 32;     // slab samples
+    const uint32_t span = (SM_COLS - 1) * hop + ksteps * 4;
+    for (uint32_t i = threadIdx.x; i < ksteps * nt_pad * 32; i += blockDim.x) {
+        const uint32_t l = i & 31, q = (i >> 5) % nt_pad, ks = (i >> 5) / nt_pad;
+        const uint32_t k = ks * 4 + (l & 3), n = q * 8 + (l >> 2), b = n >> 1;
+        bs[i] = (k < frame && b < nb) ? tw[((uint64_t)(b_first + b) * frame + k) * 2 + (n & 1)] : 0.0;
+    }
+    const uint32_t row = lane >> 2, kq = lane & 3;
+    for (uint64_t c0 = (uint64_t)blockIdx.x * SM_COLS; c0 < n_cols;
+         c0 += (uint64_t)gridDim.x * SM_COLS) {
+        __syncthreads();
+        const uint64_t s0 = c0 * hop;
+        for (uint32_t i = threadIdx.x; i < span; i += blockDim.x)
+            xs[i] = (s0 + i < n_samples) ? (double)x[s0 + i] : 0.0;
+        __syncthreads();
+        const uint32_t cl0 = warp * SM_MT * 8 + row;      // this lane's A row, m-tile 0
+        for (uint32_t gq = 0; gq < ngroups; ++gq) {
+            double acc[SM_MT][4][2];
+#pragma unroll
+            for (int mt = 0; mt < SM_MT; ++mt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[mt][q][0] = acc[mt][q][1] = 0.0;
+            const double* bq = bs + (uint64_t)gq * 4 * 32 + lane;
+            for (uint32_t ks = 0; ks < ksteps; ++ks) {
+                const uint32_t k = ks * 4 + kq;
+                double a[SM_MT], b[4];
+#pragma unroll
+                for (int mt = 0; mt < SM_MT; ++mt)
+                    a[mt] = k < frame ? xs[(cl0 + mt * 8) * hop + k] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) b[q] = bq[((uint64_t)ks * nt_pad + q) * 32];
+#pragma unroll
+                for (int mt = 0; mt < SM_MT; ++mt)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dmma_8x8x4(acc[mt][q][0], acc[mt][q][1], a[mt], b[q]);
+            }
+#pragma unroll
+            for (int mt = 0; mt < SM_MT; ++mt) {
+                const uint64_t c = c0 + cl0 + mt * 8;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t bin = (gq * 4 + q) * 4 + kq;
+                    if (c < n_cols && bin < nb) {
+                        const double re = acc[mt][q][0], im = acc[mt][q][1];
+                        // power = re^2 + im^2 (no contraction), log10 in f64, stored f32
+                        const double pw = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+                        out[c * ld_out + b_first + bin] = (float)log10(__dadd_rn(pw, 1e-12));
+                    }
+                }
+            }
+        }
+    }
+}
+
 // --------------------------------------------------------------- windows
 struct WinGeom {
     uint64_t n_cols, lag, win, win0, n_win;
@@ -1411,6 +1499,30 @@ int qs_fp_band_stft(const void* x_dev, int x_is_f32, uint64_t n_samples, uint32_
     while (chunk > 1 && span_bytes + (size_t)chunk * frame * 16 > 200 * 1024) chunk = (chunk + 1) / 2;
     QS_ARG(span_bytes + (size_t)chunk * frame * 16 <= 200 * 1024, "STFT frame too long");
     cudaStream_t st = (cudaStream_t)stream;
+    // tensor-core path (default): bins in chunks of 16 (4 n-tiles), twiddles
+    // for the whole frame + one slab of samples in shared memory
+    static const char* sk = getenv("QS_STFT_KERNEL");
+    const bool fma_path = sk && sk[0] == 'f';
+    const uint32_t ksteps = (frame + 3) / 4;
+    const size_t mma_smem = (size_t)ksteps * 4 * 32 * 8 + ((size_t)(SM_COLS - 1) * hop + ksteps * 4) * 8;
+    if (!fma_path && mma_smem <= 200 * 1024) {
+        const uint64_t slabs = (n_cols + SM_COLS - 1) / SM_COLS;
+        const unsigned mgrid = (unsigned)(slabs < 148 * 2 * 8 ? slabs : 148 * 2 * 8);
+        for (uint32_t b0 = 0; b0 < nb; b0 += 16) {
+            const uint32_t nbc = min(16u, nb - b0);
+            if (x_is_f32) {
+                QS_CUDA(cudaFuncSetAttribute(k_band_stft_mma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mma_smem), "attr");
+                k_band_stft_mma<float><<<mgrid, SM_WARPS * 32, mma_smem, st>>>(
+                    (const float*)x_dev, n_samples, frame, hop, n_cols, nbc, tw_dev, out_dev, b0, nb);
+            } else {
+                QS_CUDA(cudaFuncSetAttribute(k_band_stft_mma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mma_smem), "attr");
+                k_band_stft_mma<double><<<mgrid, SM_WARPS * 32, mma_smem, st>>>(
+                    (const double*)x_dev, n_samples, frame, hop, n_cols, nbc, tw_dev, out_dev, b0, nb);
+            }
+            QS_CHECK_LAUNCH("k_band_stft_mma");
+        }
+        return QS_OK;
+    }
     const uint64_t blocks = (n_cols + STFT_COLS - 1) / STFT_COLS;
     const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
     for (uint32_t b0 = 0; b0 < nb; b0 += chunk) {
