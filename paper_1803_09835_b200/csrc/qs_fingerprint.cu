@@ -799,6 +799,7 @@ constexpr size_t WC_OFF_LL2 = WC_OFF_LL1 + 512 * 8, WC_OFF_LL3 = WC_OFF_LL2 + 12
 constexpr size_t WC_OFF_TAB = WC_OFF_LL3 + 64 * 8;
 constexpr size_t WC_SMEM = WC_OFF_TAB + (32 * WC_FT + WC_NWID * 64 * WC_TT) * 12 + 64;
 
+template <int MODE>
 __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
     const float* __restrict__ band, WinGeom g, const int64_t* __restrict__ widx,
     const int32_t* __restrict__ wf_off, const int32_t* __restrict__ wf_idx,
@@ -818,10 +819,23 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
     int32_t* fi = (int32_t*)(tv + WC_NWID * 64 * WC_TT);
     int32_t* ti = fi + 32 * WC_FT;
     __shared__ uint32_t s_nf, s_wcnt[WC_W], s_wcnt2[WC_W], s_ncur;
-    __shared__ uint32_t s_dsel;
+    __shared__ uint32_t s_dsel, s_ninel;
     __shared__ uint64_t s_kmax, s_kmin;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
-    const uint32_t nwid = g.wmax - g.wmin + 1, nb = g.nb, mode = g.mode;
+    const uint32_t nwid = g.wmax - g.wmin + 1, nb = g.nb;
+    constexpr uint32_t mode = MODE;
+    // ineligible coefficients (MAD == 0) have select key 0; the histogram
+    // passes count them into digit 0 whenever the decided prefix is 0 and the
+    // scan takes them back out (no per-key eligibility test)
+    if (MODE == 3) {
+        if (threadIdx.x == 0) s_ninel = 0;
+        __syncthreads();
+        uint32_t ni = 0;
+        for (uint32_t j = threadIdx.x; j < WC_N; j += WC_T) ni += !(__ldg(mad + j) > 0.0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ni += __shfl_xor_sync(0xffffffffu, ni, o);
+        if (lane == 0 && ni) atomicAdd(&s_ninel, ni);
+    }
     for (uint32_t q = threadIdx.x; q < 32 * WC_FT; q += WC_T) {
         const uint32_t r = q / WC_FT, t = q - r * WC_FT;
         const int32_t e = wf_off[r] + (int32_t)t;
@@ -980,10 +994,13 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
             const uint32_t j = (threadIdx.x >> 4) * 64 + (threadIdx.x & 15);
             emit(j, (double)c3[threadIdx.x]);
         }
-        // select histograms (3 x 256, triple-buffered) and the <= 32-candidate
-        // list live in the time-resample scratch, free after level 1
+        // select histograms (3 x (256 + a trash bin for keys off the decided
+        // prefix), triple-buffered) and the <= 32-candidate list live in the
+        // time-resample scratch, free after level 1
+        constexpr uint32_t HS = 272;
         uint32_t* H = (uint32_t*)tmp;
-        uint64_t* clist = (uint64_t*)(H + 3 * 256);
+        uint64_t* clist = (uint64_t*)(H + 3 * HS);
+        const uint32_t n_inel = s_ninel;
         H[threadIdx.x] = 0;
         // CTA-wide non-finite flag, key range
 #pragma unroll
@@ -1023,12 +1040,25 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         uint32_t krem = g.top_k, gt = 0;
         uint64_t thr = 0;
         for (uint32_t pass = 0;; ++pass) {
-            uint32_t* hc = H + (pass % 3) * 256;
-            uint32_t* hn = H + ((pass + 1) % 3) * 256;
+            uint32_t* hc = H + (pass % 3) * HS;
+            uint32_t* hn = H + ((pass + 1) % 3) * HS;
+            if (shift >= 32) {  // digit and decided bits in the high words
+                // the sign (bit 31 of the high word) is masked out of dh; digits
+                // stay below it (shift <= 55)
+                const uint32_t dh = (uint32_t)(decided >> 32) & 0x7FFFFFFFu;
+                const uint32_t ph = (uint32_t)(prefix >> 32);
+                const uint32_t sh = (uint32_t)shift - 32;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint64_t k = kr[q] & ~WC_SIGN;
-                if (k && (k & decided) == prefix) atomicAdd(&hc[(uint32_t)(k >> shift) & 0xFFu], 1u);
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t h = (uint32_t)(kr[q] >> 32);
+                    atomicAdd(&hc[(h & dh) == ph ? (h >> sh) & 0xFFu : 256u], 1u);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint64_t k = kr[q] & ~WC_SIGN;
+                    atomicAdd(&hc[(k & decided) == prefix ? (uint32_t)(k >> shift) & 0xFFu : 256u], 1u);
+                }
             }
             hn[threadIdx.x] = 0;
             if (threadIdx.x == 0) s_ncur = 0;
@@ -1038,10 +1068,10 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
             {
                 uint32_t c[8], sum = 0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    c[e] = hc[8 * lane + e];
-                    sum += c[e];
-                }
+                for (int e = 0; e < 8; ++e) c[e] = hc[8 * lane + e];
+                if (lane == 0 && prefix == 0) c[0] -= n_inel;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) sum += c[e];
                 uint32_t x = sum;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -1587,13 +1617,14 @@ int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int
     }
     if (kind == 0 && mode >= 1 && F == 32 && T == WC_T64 && nb <= 16 && n_levels == 6 && wmax <= 128 &&
         wmax - wmin + 1 <= WC_NWID && (size_t)wmax * nb * 4 <= WC_N * 8) {
-        QS_CUDA(cudaFuncSetAttribute(k_win_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        auto kern = mode == 3 ? k_win_cta<3> : (mode == 2 ? k_win_cta<2> : k_win_cta<1>);
+        QS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)WC_SMEM), "attr");
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_win_cta, WC_T, WC_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WC_T, WC_SMEM);
         const uint64_t cap = (uint64_t)num_sms_fp() * (per_sm < 1 ? 1 : per_sm) * 4;
         const unsigned grid = (unsigned)(n_win < cap ? n_win : cap);
-        k_win_cta<<<grid, WC_T, WC_SMEM, (cudaStream_t)stream>>>(
+        kern<<<grid, WC_T, WC_SMEM, (cudaStream_t)stream>>>(
             band_dev, g, widx_dev, wf_off, wf_idx, wf_val, wt_off, wt_idx, wt_val, med_dev, mad_dev,
             out_dev, flags_dev);
         QS_CHECK_LAUNCH("k_win_cta");
