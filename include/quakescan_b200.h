@@ -399,6 +399,13 @@ int qs_fp_windows(const float* band_dev, uint64_t n_cols, uint32_t nb, const int
 int qs_fp_mad(const float* cols_dev, uint32_t n_coeffs, uint64_t S, double* med_dev,
               double* mad_dev, double* ws_dev, void* stream);
 
+/* Transpose of a (rows, cols) float32 row-major matrix into (cols, rows): the
+ * MAD sample pass writes one coefficient row per sampled window (coalesced)
+ * and qs_fp_mad reads one column per coefficient (estimate_mad,
+ * fingerprint.py:364-384 stacks the sampled windows the same way). */
+int qs_fp_transpose_f32(const float* src_dev, uint64_t rows, uint32_t cols, float* dst_dev,
+                        void* stream);
+
 /* topk_bits (fingerprint.py:433-466) of B rows of n coefficients (float32, or
  * float64 with is_f64). */
 int qs_fp_topk_bits(const void* coeffs_dev, int is_f64, uint64_t B, uint32_t n,

@@ -92,6 +92,7 @@ SIGNATURES = {
                              _p, _p, _p, _u32, _u32, _u32, _u32, _p, _u32, _int, _p, _p, _u32, _p,
                              _p, _p]),
     "qs_fp_mad": (_int, [_p, _u32, _u64, _p, _p, _p, _p]),
+    "qs_fp_transpose_f32": (_int, [_p, _u64, _u32, _p, _p]),
     "qs_fp_topk_bits": (_int, [_p, _int, _u64, _u32, _p, _p, _u32, _p, _p, _p]),
     "qs_fp_haar2d": (_int, [_p, _u64, _u32, _u32, _p, _u32, _int, _p]),
     "qs_fp_normalize": (_int, [_p, _int, _u64, _u32, _p, _p, _p, _p]),

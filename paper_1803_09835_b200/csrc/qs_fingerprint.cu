@@ -892,7 +892,8 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         __syncthreads();
         bool nonfinite = false;
         uint64_t kmax = 0, kmin = ~0ull;
-        auto emit = [&](uint32_t j, double v) {
+        // md / me: the column's MAD and median (mode 3), loaded ahead by the caller
+        auto emit_p = [&](uint32_t j, double v, double md, double me) {
             const float c = (float)v;  // coefficients are stored float32 (fingerprint.py:334)
             if (mode == 1) {
                 ((float*)out)[wi * WC_N + j] = c;
@@ -901,10 +902,9 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
             } else {
                 const double cd = (double)c;
                 if (!isfinite(cd)) nonfinite = true;
-                const double md = __ldg(mad + j);
                 uint64_t k = 0;
                 if (md > 0.0) {
-                    const double sc = __ddiv_rn(__dsub_rn(cd, __ldg(med + j)), md);
+                    const double sc = __ddiv_rn(__dsub_rn(cd, me), md);
                     const uint64_t m = mag_key(sc) + 1;
                     kmax = m > kmax ? m : kmax;
                     kmin = m < kmin ? m : kmin;
@@ -912,6 +912,10 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
                 }
                 keys[j] = k;
             }
+        };
+        auto emit = [&](uint32_t j, double v) {
+            if (mode == 3) emit_p(j, v, __ldg(mad + j), __ldg(med + j));
+            else emit_p(j, v, 0.0, 0.0);
         };
         auto bfly = [&](double x00, double x01, double x10, double x11, uint32_t bi, uint32_t bj,
                         uint32_t h, uint32_t w) -> double {
@@ -925,6 +929,13 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         // level 1 (32 x 64): block (bi, bj) = pixels rows 2bi, 2bi+1, cols 2bj, 2bj+1
         for (uint32_t bk = threadIdx.x; bk < 512; bk += WC_T) {
             const uint32_t bi = bk >> 5, bj = bk & 31;
+            // the block's three detail coefficients: statistics loaded ahead
+            const uint32_t j0 = bi * 64 + 32 + bj, j1 = (16 + bi) * 64 + bj, j2 = j1 + 32;
+            double pmd[3] = {0.0, 0.0, 0.0}, pme[3] = {0.0, 0.0, 0.0};
+            if (mode == 3) {
+                pmd[0] = __ldg(mad + j0); pmd[1] = __ldg(mad + j1); pmd[2] = __ldg(mad + j2);
+                pme[0] = __ldg(med + j0); pme[1] = __ldg(med + j1); pme[2] = __ldg(med + j2);
+            }
             double x[2][2];
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
@@ -938,7 +949,14 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
                     x[a][b] = (double)(float)acc;  // images are float32 (fingerprint.py:239-241)
                 }
             }
-            ll1[bk] = bfly(x[0][0], x[0][1], x[1][0], x[1][1], bi, bj, 32, 64);
+            const double lo0 = __dmul_rn(__dadd_rn(x[0][0], x[0][1]), s2);
+            const double hi0 = __dmul_rn(__dsub_rn(x[0][0], x[0][1]), s2);
+            const double lo1 = __dmul_rn(__dadd_rn(x[1][0], x[1][1]), s2);
+            const double hi1 = __dmul_rn(__dsub_rn(x[1][0], x[1][1]), s2);
+            emit_p(j0, __dmul_rn(__dadd_rn(hi0, hi1), s2), pmd[0], pme[0]);
+            emit_p(j1, __dmul_rn(__dsub_rn(lo0, lo1), s2), pmd[1], pme[1]);
+            emit_p(j2, __dmul_rn(__dsub_rn(hi0, hi1), s2), pmd[2], pme[2]);
+            ll1[bk] = __dmul_rn(__dadd_rn(lo0, lo1), s2);
         }
         __syncthreads();
         if (threadIdx.x < 128) {  // level 2 (16 x 32)
@@ -1162,14 +1180,20 @@ __global__ void __launch_bounds__(WC_T, 4) k_win_cta(
         __syncthreads();
         uint32_t pos = 0;
         for (uint32_t w = 0; w < warp; ++w) pos += s_wcnt2[w];
-        uint32_t* ob = (uint32_t*)out + wi * g.top_k;
+        // staged in the key array (the keys are in registers), then one
+        // coalesced row store; the next window's band rows overwrite it only
+        // after the loop-top barrier
+        uint32_t* sb = (uint32_t*)keys;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const uint32_t j = 256 * warp + 32 * q + lane;
             if ((takes[q] >> lane) & 1u)
-                ob[pos + __popc(takes[q] & lt)] = 2 * j + (uint32_t)(kr[q] >> 63);
+                sb[pos + __popc(takes[q] & lt)] = 2 * j + (uint32_t)(kr[q] >> 63);
             pos += __popc(takes[q]);
         }
+        __syncthreads();
+        uint32_t* ob = (uint32_t*)out + wi * g.top_k;
+        for (uint32_t i = threadIdx.x; i < g.top_k; i += WC_T) ob[i] = sb[i];
     }
 }
 
@@ -1369,6 +1393,27 @@ __global__ void __launch_bounds__(MS_T) k_col_median(const float* __restrict__ c
         v = (v + v2) / 2.0;  // np.median of an even count
     }
     if (threadIdx.x == 0) out[col] = v;
+}
+
+// (rows, cols) -> (cols, rows) through 32 x 33 shared-memory tiles; grid.x over
+// row tiles (up to 2^31), grid.y over column tiles
+__global__ void __launch_bounds__(256) k_transpose_f32(const float* __restrict__ src, uint64_t rows,
+                                                       uint32_t cols, float* __restrict__ dst) {
+    __shared__ float tile[32][33];
+    const uint64_t r0 = (uint64_t)blockIdx.x * 32;
+    const uint32_t c0 = blockIdx.y * 32;
+    const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (uint32_t k = 0; k < 32; k += 8) {
+        const uint64_t r = r0 + ty + k;
+        if (r < rows && c0 + tx < cols) tile[ty + k][tx] = src[r * cols + c0 + tx];
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < 32; k += 8) {
+        const uint32_t c = c0 + ty + k;
+        if (c < cols && r0 + tx < rows) dst[(uint64_t)c * rows + r0 + tx] = tile[tx][ty + k];
+    }
 }
 
 __global__ void k_mid_mean(const double* __restrict__ a, const double* __restrict__ b, uint32_t n,
@@ -1669,6 +1714,17 @@ int qs_fp_mad(const float* cols_dev, uint32_t n_coeffs, uint64_t S, double* med_
         }
     }
     QS_CHECK_LAUNCH("qs_fp_mad");
+    return QS_OK;
+}
+
+int qs_fp_transpose_f32(const float* src_dev, uint64_t rows, uint32_t cols, float* dst_dev,
+                        void* stream) {
+    if (rows == 0 || cols == 0) return QS_OK;
+    QS_ARG(src_dev && dst_dev && src_dev != dst_dev, "transpose needs two distinct buffers");
+    QS_ARG(cols <= 65535u * 32u, "too many columns");
+    const dim3 grid((unsigned)((rows + 31) / 32), (cols + 31) / 32);
+    k_transpose_f32<<<grid, 256, 0, (cudaStream_t)stream>>>(src_dev, rows, cols, dst_dev);
+    QS_CHECK_LAUNCH("k_transpose_f32");
     return QS_OK;
 }
 

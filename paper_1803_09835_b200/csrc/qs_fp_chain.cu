@@ -186,6 +186,7 @@ struct Dev {
     double *wf_val, *wt_val, *mws;
     uint32_t* flags;
     float* cols;
+    float* rows;  // the MAD sample, one coefficient row per window (transposed into cols)
 };
 
 void carve(Bump& a, const Geo& g, const Tables& tb, uint64_t n_sample, Dev& d) {
@@ -201,6 +202,7 @@ void carve(Bump& a, const Geo& g, const Tables& tb, uint64_t n_sample, Dev& d) {
     d.flags = a.take<uint32_t>(4);
     d.mws = a.take<double>(2 * (uint64_t)g.F * g.T);
     d.cols = a.take<float>((uint64_t)g.F * g.T * n_sample);
+    d.rows = a.take<float>((uint64_t)g.F * g.T * n_sample);
 }
 
 template <class T>
@@ -273,8 +275,9 @@ int qs_fingerprint_chain(const void* x_dev, int x_is_f32, uint64_t n_samples,
         QS_ARG(n_mad_sample >= 1 && n_mad_sample <= g.n_win, "MAD sample size out of range");
         QS_TRY(qs_fp_windows(d.band, g.n_cols, g.nb, mad_sample_dev, 0, n_mad_sample, g.lag, g.win,
                              g.frame, g.hop, d.wf_off, d.wf_idx, d.wf_val, d.wt_off, d.wt_idx,
-                             d.wt_val, g.wmin, g.wmax, g.F, g.T, d.sched, nlev, 2, nullptr, nullptr,
-                             0, d.cols, d.flags, stream));
+                             d.wt_val, g.wmin, g.wmax, g.F, g.T, d.sched, nlev, 1, nullptr, nullptr,
+                             0, d.rows, d.flags, stream));
+        QS_TRY(qs_fp_transpose_f32(d.rows, n_mad_sample, nc, d.cols, stream));
         QS_TRY(qs_fp_mad(d.cols, nc, n_mad_sample, med_dev, mad_dev, d.mws, stream));
     }
     // top_k must not exceed the coefficients with a nonzero MAD (fingerprint.py:448-451)

@@ -428,8 +428,13 @@ def _mad_from_chain(ch, params, rate, seed, total):
         rng = np.random.default_rng(seed)
         sample = np.sort(rng.choice(total, size=n_sample, replace=False))
     n_coeffs = params.n_coeffs
+    # one coefficient row per sampled window (coalesced stores), then one
+    # transpose into the per-coefficient columns the order statistics read
+    rows = torch.empty((n_sample, n_coeffs), dtype=torch.float32, device="cuda")
+    ch.windows(1, rows, widx=torch.from_numpy(sample.astype(np.int64)).cuda(), n=n_sample)
     cols = torch.empty((n_coeffs, n_sample), dtype=torch.float32, device="cuda")
-    ch.windows(2, cols, widx=torch.from_numpy(sample.astype(np.int64)).cuda(), n=n_sample)
+    nat.call("qs_fp_transpose_f32", nat.ptr(rows), n_sample, n_coeffs, nat.ptr(cols), nat.stream())
+    del rows
     med = torch.empty(n_coeffs, dtype=torch.float64, device="cuda")
     mad = torch.empty(n_coeffs, dtype=torch.float64, device="cuda")
     ws = torch.empty(2 * n_coeffs, dtype=torch.float64, device="cuda")
