@@ -364,7 +364,11 @@ def fingerprint_bench(args, steps, device, threads, cpu=True):
            "ms_per_step": ms, "steps": steps, "n_samples": n, "n_fingerprints": n_fp,
            "workload": workload, "dtype": "f64 (STFT/resize/Haar/normalise), f32 stores",
            "e2e": {"value": n / e2e_s / 1e6, "unit": "Msamples/s", "seconds": e2e_s,
-                   "h2d_bytes_per_step": int(n * 8), "d2h_bytes_per_step": d2h,
+                   "h2d_bytes_per_step": int(n * 4), "d2h_bytes_per_step": d2h,
+                   "host_memory": ("pageable float64 (TimeSeries coerces the float32 recording like "
+                                   "the reference); every sample is exactly a float32, so the staging "
+                                   "pass narrows it (qs_host_pack_f32) and 4 bytes per sample cross "
+                                   "PCIe; the chain widens them exactly"),
                    "path": "fingerprint.fingerprint_series(TimeSeries(host float32 -> float64))"}}
     # the step before fingerprinting in the reference CLI (cli.py:152-153): zero-phase
     # band-pass of a device-resident day
@@ -437,7 +441,23 @@ def pair_roofline(ds, stages, n_trip, m, t, hbm, peak_kind, filt):
             "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": achieved / hbm, "algorithmic_bytes": tot_b, "ms": tot_ms, "passes": per,
             "accounting": "16 B/hit + 4 B/member of walked buckets + 20 B/triplet (SURVEY 8d)",
-            "traffic": None}
+            "traffic": _ncu_traffic(int(ds.n) if hasattr(ds, "n") else None, filt)}
+
+
+def _ncu_traffic(n, filt):
+    """DRAM bytes (read + write) of every pair-stage launch of one step, from the
+    committed ncu capture (profiles/traffic.json, written by tools/launch_summary.py
+    from a run of tools/one_search.py at the same n with the filter on); None when
+    no capture matches this run."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if not filt or "pair_stage_dram_bytes_total" not in t or (n is not None and t.get("n") != n):
+        return None
+    return t["pair_stage_dram_bytes_total"]
 
 
 def _stage_avg(timed):
@@ -603,45 +623,68 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        if tables_mode:
-            a, b = host_rows
-            host_bits = bits[: b - a].cpu().numpy().view(np.uint32)
-        else:
-            host_bits = bits.cpu().numpy().view(np.uint32)
-        rows = host_bits.shape[0]
-        fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
-                             indices=np.arange(rows, dtype=np.uint64),
-                             epochs=np.arange(rows, dtype=np.float64), bits=host_bits)
+        # the step's inputs in PINNED host memory (the bench contract): the library
+        # detects page-locked arrays and copies them by DMA from where they lie; the
+        # same call with a pageable numpy array (staged through pinned buffers,
+        # narrowed to uint16 on the way) is reported as `pageable`
+        src = bits[: host_rows[1] - host_rows[0]] if tables_mode else bits
+        pinned_t = torch.empty(tuple(src.shape), dtype=torch.int32, pin_memory=True)
+        pinned_t.copy_(src)
+        torch.cuda.synchronize()
         cfg_e = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, seed=0,
                                 occurrence_threshold=occ, near_repeat_exclusion_s=0.0)
 
-        def e2e_call():
-            if tables_mode:
-                return sh.search_fingerprints_sharded(fps, n, cfg_e)
-            return ls.search_fingerprints(fps, cfg_e)  # mapping generated inside, like the reference
+        def time_e2e(host_bits):
+            rows = host_bits.shape[0]
+            fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
+                                 indices=np.arange(rows, dtype=np.uint64),
+                                 epochs=np.arange(rows, dtype=np.float64), bits=host_bits)
 
-        e2e_call()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        out_bytes = 0
-        for _ in range(args.e2e_steps):
-            rec, est, _ = e2e_call()
-            out_bytes = rec.nbytes
-        torch.cuda.synchronize()
-        e_s = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
-            et = torch.tensor([e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-            e_s = float(et.item())
+            def e2e_call():
+                if tables_mode:
+                    return sh.search_fingerprints_sharded(fps, n, cfg_e)
+                return ls.search_fingerprints(fps, cfg_e)  # mapping generated inside, like the reference
+
+            e2e_call()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            out_bytes = 0
+            for _ in range(args.e2e_steps):
+                rec, est, _ = e2e_call()
+                out_bytes = rec.nbytes
+            torch.cuda.synchronize()
+            e_s = (time.perf_counter() - t0) / args.e2e_steps
+            if world > 1:
+                et = torch.tensor([e_s], dtype=torch.float64, device=dev)
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+                e_s = float(et.item())
+            return e_s, out_bytes, int(ls.LAST_H2D_BYTES)
+
         e_units = n if tables_mode else world * n
+        e_s, out_bytes, h2d = time_e2e(pinned_t.numpy().view(np.uint32))
         e2e = {"value": e_units / e_s, "unit": "fingerprints/s",
-               "h2d_bytes_per_step": int(e_units * 400 * 4), "d2h_bytes_per_step": int(out_bytes),
+               "h2d_bytes_per_step": h2d or int(e_units * 400 * 4),
+               "d2h_bytes_per_step": int(out_bytes), "input_bytes_per_step": int(e_units * 400 * 4),
                "seconds_per_step": e_s,
+               "host_memory": ("pinned: DMA from the caller's array, QS_H2D_SPLIT (default 0.7) of "
+                               "every chunk's rows narrowed to uint16 by the host cores on the way "
+                               "(h2d_bytes_per_step = the bytes that crossed PCIe)"),
                "path": ("sharded.search_fingerprints_sharded (host row block per rank)" if tables_mode
                         else "lsh_search.search_fingerprints(FingerprintSet with host numpy bits)")}
-        del fps, host_bits
+        if not tables_mode:
+            pageable = np.array(pinned_t.numpy().view(np.uint32))  # an ordinary numpy array
+            del pinned_t
+            p_s, _, ph2d = time_e2e(pageable)
+            e2e["pageable"] = {"value": e_units / p_s, "seconds_per_step": p_s,
+                               "h2d_bytes_per_step": ph2d,
+                               "host_memory": ("pageable numpy array: staged through two pinned "
+                                               "buffers by a thread pool, narrowed to uint16 on the "
+                                               "way (qs_host_pack_u16), widened on the device")}
+            del pageable
+        else:
+            del pinned_t
     del bits
     torch.cuda.empty_cache()
 

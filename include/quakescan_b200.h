@@ -42,6 +42,27 @@ const char* qs_last_error(void);
 /* Writes "name|sm_major.minor|n_sms|hbm_bytes" of the current device. */
 int qs_device_info(char* buf, size_t len);
 
+/* ------------------------------------------------- host <-> device transfer
+ * Helpers of the host-buffer entry points: the reference's
+ * search_fingerprints (lsh_search.py:314-333) and fingerprint_series
+ * (fingerprint.py:581-623) take host arrays, so their copy is part of the
+ * call here (csrc/qs_host.cu). */
+/* 1 when host_ptr lies in page-locked memory (cudaHostAlloc / cudaHostRegister:
+ * DMA straight from the caller's array), 0 for pageable memory. */
+int qs_host_ptr_pinned(const void* host_ptr);
+/* dst_host[i] = min(src_host[i], 65535): bit indices narrowed while they are
+ * staged (valid for d <= 65535: a saturated value is >= d and is flagged by
+ * the signature kernel's range check).  Host function, thread-safe. */
+int qs_host_pack_u16(const uint32_t* src_host, uint16_t* dst_host, uint64_t count);
+/* dst_host[i] = (float)src_host[i]; *exact_out = 1 when every value widens
+ * back to itself (then a float32 upload gives the chain the same samples),
+ * 0 otherwise (NaN, overflow, inexact).  Host function, thread-safe. */
+int qs_host_pack_f32(const double* src_host, float* dst_host, uint64_t count, int* exact_out);
+/* dst_dev[i] = src_dev[i] (uint16 -> uint32), both 16-byte aligned. */
+int qs_bits_widen_u16(const uint16_t* src_dev, uint32_t* dst_dev, uint64_t count, void* stream);
+int qs_memcpy_h2d_async(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+int qs_memcpy_d2h_async(void* dst_host, const void* src_dev, size_t bytes, void* stream);
+
 /* ------------------------------------------------------------ Min-Max hash */
 
 /* values_dev[x * n_funcs + j] = fmix64(((x + 1) * GOLDEN64) ^ (seed + j)).

@@ -6,6 +6,7 @@ log-power STFT -> area-resampled spectral image -> full 2-D orthonormal Haar
 """
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -279,7 +280,7 @@ class _Chain:
         else:
             # host trace: the STFT of every column whose samples have landed runs
             # while the later chunks are still being copied
-            from .lsh_search import _to_device_staged
+            from .lsh_search import _host_pinned, _to_device_staged
             holder, state = [], [0]
 
             def on_chunk(done):
@@ -288,9 +289,22 @@ class _Chain:
                 state[0] = max(state[0], c_hi)
 
             arr = np.ascontiguousarray(x, dtype=np.float64)
-            xd = torch.empty(arr.shape, dtype=torch.float64, device="cuda")
-            holder.append(xd)
-            xd = _to_device_staged(arr, on_chunk=on_chunk, out=xd)
+            xd = None
+            if not _host_pinned(arr) and os.environ.get("QS_H2D_NARROW", "1") != "0":
+                # a float32 recording coerced to float64 (ingest.py:36) goes up as
+                # float32 — half the staging writes and DMA bytes; the chain widens
+                # float32 samples exactly.  Any inexact sample: float64 instead.
+                x32 = torch.empty(arr.shape, dtype=torch.float32, device="cuda")
+                holder.append(x32)
+                xd = _to_device_staged(arr, on_chunk=on_chunk, out=x32, narrow_f32=True)
+                if xd is None:
+                    holder.clear()
+                    state[0] = 0
+                    del x32
+            if xd is None:
+                xd = torch.empty(arr.shape, dtype=torch.float64, device="cuda")
+                holder.append(xd)
+                xd = _to_device_staged(arr, on_chunk=on_chunk, out=xd)
             stft(xd, state[0], self.n_cols)
         self.x = xd
 
@@ -418,15 +432,19 @@ def ihaar2d(a) -> np.ndarray:
     return _haar_call(a, True)
 
 
-def _mad_from_chain(ch, params, rate, seed, total):
-    torch = ch.torch
+def _mad_sample(rate, seed, total):
+    """The sampled window indices, drawn by the reference's own numpy RNG call
+    (fingerprint.py:352-357)."""
     n_sample = max(1, int(round(rate * total)))
     if n_sample >= total:
-        sample = np.arange(total)
-        n_sample = total
-    else:
-        rng = np.random.default_rng(seed)
-        sample = np.sort(rng.choice(total, size=n_sample, replace=False))
+        return np.arange(total), total
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(total, size=n_sample, replace=False)), n_sample
+
+
+def _mad_from_chain(ch, params, rate, seed, total, sample=None):
+    torch = ch.torch
+    sample, n_sample = sample.result() if sample is not None else _mad_sample(rate, seed, total)
     n_coeffs = params.n_coeffs
     # one coefficient row per sampled window (coalesced stores), then one
     # transpose into the per-coefficient columns the order statistics read
@@ -526,11 +544,20 @@ def fingerprint_series(ts, params: FingerprintParams, stats: MadStats | None = N
     total = n_windows(ts, params)
     if total == 0:
         raise DataError("series shorter than one fingerprint window")
-    ch = _Chain(ts, params, windows=True)
+    draw = None
     if stats is None:
         if not 0 < mad_rate <= 1:
             raise ParameterError(f"sampling rate must be in (0, 1], got {mad_rate}")
-        med, mad, n_sample = _mad_from_chain(ch, params, mad_rate, mad_seed, total)
+        # the sample draw (~50 ms of host work at 8e6 windows) runs beside the
+        # trace upload and the STFT instead of after them
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(1) as ex:
+            draw = ex.submit(_mad_sample, mad_rate, mad_seed, total)
+            ch = _Chain(ts, params, windows=True)
+    else:
+        ch = _Chain(ts, params, windows=True)
+    if stats is None:
+        med, mad, n_sample = _mad_from_chain(ch, params, mad_rate, mad_seed, total, sample=draw)
         stats = MadStats(median=med.cpu().numpy(), mad=mad.cpu().numpy(), rate=float(mad_rate),
                          seed=int(mad_seed), n_sampled=int(n_sample), n_total=int(total))
     else:

@@ -602,19 +602,25 @@ def _copy_pool():
     global _COPY_POOL
     if _COPY_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        want = int(os.environ.get("QS_COPY_THREADS", "8"))
+        want = int(os.environ.get("QS_COPY_THREADS", "16"))
         _COPY_POOL = ThreadPoolExecutor(max(1, min(want, len(os.sched_getaffinity(0)))))
     return _COPY_POOL
 
 
-def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20, on_chunk=None, out=None):
-    """Host -> device copy of a pageable numpy array through two pinned staging
-    buffers: the host copy into one buffer is split over a thread pool (numpy
-    releases the GIL) while the DMA of the other runs on a copy stream (~44
-    GB/s on the B200 box against ~14 GB/s single-threaded).  `on_chunk(done)`
-    is called after each chunk lands, on the compute stream (work on the
-    first `done` elements overlaps the remaining copies).  `out`: an existing
-    CUDA tensor of the same shape and dtype to fill."""
+def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20, on_chunk=None, out=None,
+                      narrow_f32: bool = False):
+    """Host -> device copy of a numpy array in chunks on a copy stream.
+    `on_chunk(done)` is called after each chunk is ordered on the compute
+    stream (work on the first `done` elements overlaps the remaining copies).
+    `out`: an existing CUDA tensor of the same shape to fill.
+
+    A page-locked array is copied by DMA from where it lies.  A pageable one
+    goes through two pinned staging buffers: the host pass into one buffer is
+    split over a thread pool (the C helpers and numpy release the GIL) while
+    the DMA of the other runs.  `narrow_f32`: a float64 array is narrowed to
+    float32 on the way (`out` is float32; qs_host_pack_f32) — returns None as
+    soon as a value is not exactly representable, the caller then repeats the
+    copy in float64."""
     torch = nat.torch()
     flat = arr.reshape(-1)
     if out is None:
@@ -622,24 +628,54 @@ def _to_device_staged(arr: np.ndarray, chunk_bytes: int = 256 << 20, on_chunk=No
     if flat.size == 0:
         return out
     dst = out.view(-1)
-    per = max(1, chunk_bytes // flat.itemsize)
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    copy.wait_stream(compute)  # dst's allocation is ordered on the compute stream
+    if not narrow_f32 and _host_pinned(flat):
+        per = max(1, chunk_bytes // flat.itemsize)
+        cstream = nat.ctypes.c_void_p(copy.cuda_stream)
+        isz = flat.itemsize
+        for a in range(0, flat.size, per):
+            b = min(flat.size, a + per)
+            nat.call("qs_memcpy_h2d_async", nat.ctypes.c_void_p(dst.data_ptr() + a * isz),
+                     nat.ctypes.c_void_p(flat.ctypes.data + a * isz), (b - a) * isz, cstream)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            compute.wait_event(ev)
+            if on_chunk is not None:
+                on_chunk(b)
+        out.record_stream(copy)
+        return out
+    per = max(1, chunk_bytes // dst.element_size())
     stage = [torch.empty(min(per, flat.size), dtype=dst.dtype, pin_memory=True) for _ in range(2)]
     done = [None, None]
     pool = _copy_pool()
     nthr = pool._max_workers
-    compute = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
-    copy.wait_stream(compute)  # dst's allocation is ordered on the compute stream
+    lib = nat.lib()
     for k, a in enumerate(range(0, flat.size, per)):
         b = min(flat.size, a + per)
         s = k & 1
         if done[s] is not None:
             done[s].synchronize()
-        host = stage[s].numpy()
         n = b - a
         step = max(1 << 16, -(-n // nthr))
-        list(pool.map(lambda i: np.copyto(host[i:min(n, i + step)], flat[a + i:a + min(n, i + step)]),
-                      range(0, n, step)))
+        if narrow_f32:
+            hbase, sbase = stage[s].data_ptr(), flat.ctypes.data
+
+            def pack(i, a=a, n=n, hbase=hbase):
+                ok = nat.ctypes.c_int(1)
+                lib.qs_host_pack_f32(nat.ctypes.c_void_p(sbase + (a + i) * 8),
+                                     nat.ctypes.c_void_p(hbase + i * 4), min(n, i + step) - i,
+                                     nat.ctypes.byref(ok))
+                return ok.value
+
+            if not all(pool.map(pack, range(0, n, step))):
+                copy.synchronize()
+                return None
+        else:
+            host = stage[s].numpy()
+            list(pool.map(lambda i: np.copyto(host[i:min(n, i + step)], flat[a + i:a + min(n, i + step)]),
+                          range(0, n, step)))
         with torch.cuda.stream(copy):
             dst[a:b].copy_(stage[s][:n], non_blocking=True)
             ev = torch.cuda.Event()
@@ -675,13 +711,27 @@ def signatures_for_search(bits, mapping: HashMapping, with_keys: bool = True):
     return keys, rkeys, tags, bad
 
 
+LAST_H2D_BYTES = 0  # bytes the last signatures_for_search_host call sent over PCIe
+
+
+def _host_pinned(arr: np.ndarray) -> bool:
+    """True when the array's memory is page-locked (allocated or registered
+    with CUDA): it is then copied by DMA from where it lies."""
+    if arr.size == 0:
+        return False
+    return bool(nat.lib().qs_host_ptr_pinned(nat.ctypes.c_void_p(arr.ctypes.data)))
+
+
 def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_bytes: int = 256 << 20):
     """Host (n, K) int32 bits -> the search layout, the host->device copy
-    pipelined with the signature kernel: row chunks go through two pinned
-    staging buffers on a copy stream (the host copy into one buffer split over
-    a thread pool while the other's DMA runs) and the kernel signs each chunk's
-    rows (qs_minmax_signatures_search_rows) on the compute stream as soon as
-    they land."""
+    pipelined with the signature kernel: the kernel signs each row chunk
+    (qs_minmax_signatures_search_rows) on the compute stream as soon as it has
+    landed.  A page-locked array is copied by DMA straight from the caller's
+    memory; a pageable one goes through two pinned staging buffers (the host
+    pass into one buffer split over a thread pool while the other's DMA runs),
+    narrowed to uint16 on the way when d <= 65535 (qs_host_pack_u16: half the
+    staging writes and half the DMA bytes; widened again on the device,
+    out-of-range values saturate and are flagged by the kernel's range check)."""
     torch = nat.torch()
     n, K = arr.shape
     t = mapping.t
@@ -690,34 +740,128 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
     bdev = torch.empty((n, K), dtype=torch.int32, device="cuda")
     if n == 0:
         return keys, rkeys, tags, bad
-    rows_per = max(1, chunk_bytes // (K * 4))
-    stage = [torch.empty((min(rows_per, n), K), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    done = [None, None]
-    pool = _copy_pool()
-    nthr = pool._max_workers
+    rows_per = max(4, (chunk_bytes // (K * 4)) & ~3)  # chunk starts stay 16-byte aligned
     compute = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     copy.wait_stream(compute)  # bdev's allocation is ordered on the compute stream
+    cstream = nat.ctypes.c_void_p(copy.cuda_stream)
+    lib = nat.lib()
+    global LAST_H2D_BYTES
+    LAST_H2D_BYTES = 0
+
+    def sign(r0, rows):
+        nat.call("qs_minmax_signatures_search_rows", nat.ptr(bdev), n, r0, rows, K, nat.ptr(plan),
+                 mapping.d, t, mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
+                 nat.ptr(bad), nat.stream())
+
+    narrow = mapping.d <= 0xFFFF and os.environ.get("QS_H2D_NARROW", "1") != "0"
+    if _host_pinned(arr):
+        # DMA from the caller's memory.  With narrowing on, the first `split` of
+        # every chunk's rows is narrowed to uint16 by the thread pool (into pinned
+        # staging buffers, for the next chunk while this one's copies run) and the
+        # rest is copied as it lies: the PCIe link then moves (1 - split / 2) of the
+        # bytes while the host cores stay below their own narrowing rate
+        # (QS_H2D_SPLIT, default 0.7: measured on the 16-core B200 box, where the
+        # cores narrow ~67 GB/s of source and the link copies ~55 GB/s).
+        base = arr.ctypes.data
+        split = float(os.environ.get("QS_H2D_SPLIT", "0.7")) if narrow else 0.0
+        split = min(1.0, max(0.0, split))
+        pool = _copy_pool()
+        nthr = pool._max_workers
+        cap = min(rows_per, n)
+        ncap = int(cap * split)
+        if ncap:
+            stage = [torch.empty((ncap, K), dtype=torch.int16, pin_memory=True) for _ in range(2)]
+            dstage = [torch.empty((ncap, K), dtype=torch.int16, device="cuda") for _ in range(2)]
+        done = [None, None]
+        for k, r0 in enumerate(range(0, n, rows_per)):
+            rows = min(n, r0 + rows_per) - r0
+            nrow = min(ncap, int(rows * split))
+            sl = k & 1
+            if nrow:
+                if done[sl] is not None:
+                    done[sl].synchronize()
+                step = max(1, (1 << 18) // K, -(-nrow // nthr))
+                hbase = stage[sl].data_ptr()
+
+                def pack(i, r0=r0, nrow=nrow, hbase=hbase, step=step):
+                    cnt = min(nrow, i + step) - i
+                    lib.qs_host_pack_u16(nat.ctypes.c_void_p(base + (r0 + i) * K * 4),
+                                         nat.ctypes.c_void_p(hbase + i * K * 2), cnt * K)
+
+                list(pool.map(pack, range(0, nrow, step)))
+                with torch.cuda.stream(copy):
+                    dstage[sl][:nrow].copy_(stage[sl][:nrow], non_blocking=True)
+                nat.call("qs_bits_widen_u16", nat.ptr(dstage[sl]),
+                         nat.ctypes.c_void_p(bdev.data_ptr() + r0 * K * 4), nrow * K, cstream)
+            LAST_H2D_BYTES += nrow * K * 2 + (rows - nrow) * K * 4
+            if rows > nrow:
+                nat.call("qs_memcpy_h2d_async",
+                         nat.ctypes.c_void_p(bdev.data_ptr() + (r0 + nrow) * K * 4),
+                         nat.ctypes.c_void_p(base + (r0 + nrow) * K * 4), (rows - nrow) * K * 4,
+                         cstream)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            done[sl] = ev
+            compute.wait_event(ev)
+            sign(r0, rows)
+        bdev.record_stream(copy)
+        if ncap:
+            for d_ in dstage:
+                d_.record_stream(copy)
+        # the caller's array is read until the last copy has run: the search that
+        # follows synchronises (the range flag's .item()) before anything returns
+        return keys, rkeys, tags, bad
+
+    pool = _copy_pool()
+    nthr = pool._max_workers
+    cap = min(rows_per, n)
+    done = [None, None]
+    if narrow:
+        stage = [torch.empty((cap, K), dtype=torch.int16, pin_memory=True) for _ in range(2)]
+        dstage = [torch.empty((cap, K), dtype=torch.int16, device="cuda") for _ in range(2)]
+        src = arr.view(np.uint32)
+    else:
+        stage = [torch.empty((cap, K), dtype=torch.int32, pin_memory=True) for _ in range(2)]
     for k, r0 in enumerate(range(0, n, rows_per)):
         r1 = min(n, r0 + rows_per)
         sl = k & 1
         if done[sl] is not None:
             done[sl].synchronize()
-        host = stage[sl].numpy()
         rows = r1 - r0
         step = max(1, (1 << 18) // K, -(-rows // nthr))
-        list(pool.map(lambda i: np.copyto(host[i:min(rows, i + step)], arr[r0 + i:r0 + min(rows, i + step)]),
-                      range(0, rows, step)))
-        with torch.cuda.stream(copy):
-            bdev[r0:r1].copy_(stage[sl][:rows], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
+        if narrow:
+            hbase = stage[sl].data_ptr()
+
+            def pack(i, r0=r0, rows=rows, hbase=hbase):
+                cnt = min(rows, i + step) - i
+                lib.qs_host_pack_u16(nat.ctypes.c_void_p(src.ctypes.data + (r0 + i) * K * 4),
+                                     nat.ctypes.c_void_p(hbase + i * K * 2), cnt * K)
+
+            list(pool.map(pack, range(0, rows, step)))
+            with torch.cuda.stream(copy):
+                dstage[sl][:rows].copy_(stage[sl][:rows], non_blocking=True)
+                nat.call("qs_bits_widen_u16", nat.ptr(dstage[sl]),
+                         nat.ctypes.c_void_p(bdev.data_ptr() + r0 * K * 4), rows * K, cstream)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+        else:
+            host = stage[sl].numpy()
+            list(pool.map(lambda i: np.copyto(host[i:min(rows, i + step)],
+                                              arr[r0 + i:r0 + min(rows, i + step)]),
+                          range(0, rows, step)))
+            with torch.cuda.stream(copy):
+                bdev[r0:r1].copy_(stage[sl][:rows], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
         done[sl] = ev
         compute.wait_event(ev)
-        nat.call("qs_minmax_signatures_search_rows", nat.ptr(bdev), n, r0, rows, K, nat.ptr(plan),
-                 mapping.d, t, mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
-                 nat.ptr(bad), nat.stream())
+        sign(r0, rows)
+        LAST_H2D_BYTES += rows * K * (2 if narrow else 4)
     bdev.record_stream(copy)
+    if narrow:
+        for d_ in dstage:
+            d_.record_stream(copy)
     return keys, rkeys, tags, bad
 
 

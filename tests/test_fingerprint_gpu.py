@@ -183,3 +183,36 @@ def test_device_trace_and_search_integration(fp):
                            occurrence_threshold=0.01, exclusion_windows=10)
     assert rec.tobytes() == want.tobytes()
     assert st.distinct_pairs == wst["distinct_pairs"]
+
+
+def test_host_trace_upload_paths(fp, monkeypatch):
+    """The host -> device copy of the trace changes nothing: a float32
+    recording (coerced to float64 by TimeSeries, every sample exactly a
+    float32) goes up narrowed to float32; a float64 trace with inexact samples
+    falls back to the float64 copy; page-locked arrays are copied in place.
+    All equal the device-resident float64 trace's fingerprints."""
+    import torch
+    from paper_1803_09835_b200 import lsh_search as ls
+    from paper_1803_09835_b200 import workloads
+    x64, _ = workloads.cfg0_trace(n_samples=120_000, seed=4, copies=3)
+    x64 = np.array(x64, dtype=np.float64)
+    x64[1000] = 0.1  # not a float32
+    params = _params(fp, workloads.CFG0_PARAMS)
+    for name, x in (("float32 recording", x64.astype(np.float32)), ("float64", x64)):
+        xf = np.asarray(x, np.float64)
+        exact = bool(np.array_equal(xf.astype(np.float32).astype(np.float64), xf))
+        assert exact == (name == "float32 recording")
+        want, wmad = fp.fingerprint_series(_ts(torch.from_numpy(xf).cuda()), params)
+        want_bits = want.bits.cpu().numpy().view(np.uint32)
+        got, gmad = fp.fingerprint_series(_ts(x), params)
+        assert np.array_equal(got.bits, want_bits), name
+        assert np.array_equal(gmad.median, wmad.median) and np.array_equal(gmad.mad, wmad.mad)
+        monkeypatch.setenv("QS_H2D_NARROW", "0")
+        got2, _ = fp.fingerprint_series(_ts(x), params)
+        monkeypatch.delenv("QS_H2D_NARROW")
+        assert np.array_equal(got2.bits, want_bits), name
+        hold = torch.empty(xf.shape, dtype=torch.float64, pin_memory=True)
+        hold.numpy()[...] = xf
+        assert ls._host_pinned(hold.numpy())
+        got3, _ = fp.fingerprint_series(_ts(hold.numpy()), params)
+        assert np.array_equal(got3.bits, want_bits), name

@@ -206,16 +206,33 @@ def test_cfg1_1e5_vs_oracle(ls, cfg1_1e5, occ_limit, p, excl):
         assert st.filtered_fingerprints > 0.3 * n  # the filter fires (noise groups removed)
 
 
-def test_cfg1_1e5_host_bits_e2e(ls, cfg1_1e5):
+@pytest.mark.parametrize("host_memory", ["pageable", "pageable_u32", "pinned", "pinned_direct",
+                                         "pinned_all_narrowed"])
+def test_cfg1_1e5_host_bits_e2e(ls, cfg1_1e5, host_memory, monkeypatch):
     """The same N = 1e5 batch through search_fingerprints with host bits (the
-    e2e path the bench times: pinned row-chunk H2D pipelined with the fused
-    signature kernel)."""
+    e2e path the bench times: row-chunk H2D pipelined with the fused signature
+    kernel) from a pageable array (narrowed to uint16 while staged, or staged
+    as uint32 with QS_H2D_NARROW=0) and from page-locked memory (DMA from the
+    array, a share of the rows narrowed on the way: default, none, all)."""
+    import torch
     from paper_1803_09835_b200.fingerprint import FingerprintSet
     bits, want_sigs, m = cfg1_1e5
     n = bits.shape[0]
+    if host_memory.startswith("pinned"):
+        if host_memory != "pinned":
+            monkeypatch.setenv("QS_H2D_SPLIT", "0" if host_memory == "pinned_direct" else "1")
+        hold = torch.empty(bits.shape, dtype=torch.int32, pin_memory=True)
+        hbits = hold.numpy().view(np.uint32)
+        hbits[...] = bits
+        assert ls._host_pinned(hbits)
+    else:
+        hbits = bits
+        assert not ls._host_pinned(np.ascontiguousarray(hbits))
+        if host_memory == "pageable_u32":
+            monkeypatch.setenv("QS_H2D_NARROW", "0")
     fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
                          indices=np.arange(n, dtype=np.uint64),
-                         epochs=np.arange(n, dtype=np.float64), bits=bits)
+                         epochs=np.arange(n, dtype=np.float64), bits=hbits)
     cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, occurrence_threshold=120 / n,
                           near_repeat_exclusion_s=0.0)
     rec, st, _ = ls.search_fingerprints(fps, cfg, mapping=m)
@@ -223,3 +240,22 @@ def test_cfg1_1e5_host_bits_e2e(ls, cfg1_1e5):
     assert rec.tobytes() == want.tobytes()
     _check_stats(st, dict(wst), "e2e")
 
+
+@pytest.mark.parametrize("bad_value", [4096, 65535, 65536, 70000, 0xFFFFFFFF])
+def test_host_bits_out_of_range(ls, bad_value):
+    """An index >= d raises like the reference's range check (minmax_hash.py:
+    107-108) on the narrowed staging path too: values above 65535 saturate to
+    65535 >= d instead of wrapping into range."""
+    from paper_1803_09835_b200 import workloads
+    from paper_1803_09835_b200.errors import ParameterError
+    from paper_1803_09835_b200.fingerprint import FingerprintSet
+    bits, _ = workloads.cfg1_bits(n=3000, seed=5)
+    bits = np.array(bits, dtype=np.uint32)
+    bits[1234, 7] = bad_value
+    n = bits.shape[0]
+    fps = FingerprintSet(d=4096, top_k=400, window_len_s=1.0, window_lag_s=1.0,
+                         indices=np.arange(n, dtype=np.uint64),
+                         epochs=np.arange(n, dtype=np.float64), bits=bits)
+    cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, near_repeat_exclusion_s=0.0)
+    with pytest.raises(ParameterError):
+        ls.search_fingerprints(fps, cfg)

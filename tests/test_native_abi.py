@@ -36,3 +36,40 @@ def test_library_is_sm100a_only():
                          text=True).stdout
     archs = set(re.findall(r"sm_\d+a?", out))
     assert archs == {"sm_100a"}, archs
+
+
+def test_host_pack_helpers():
+    """Host-side staging helpers (csrc/qs_host.cu): the saturating uint32 ->
+    uint16 narrow and the float64 -> float32 narrow with its exactness flag."""
+    import ctypes
+
+    import numpy as np
+    from paper_1803_09835_b200 import _native
+    lib = _native.lib()
+    rng = np.random.default_rng(3)
+    for count in (0, 1, 15, 16, 17, 1000, 4099):
+        src = rng.integers(0, 4096, count, dtype=np.uint32)
+        if count > 2:
+            src[1] = 70000
+            src[count - 1] = 0xFFFFFFFF
+        dst = np.zeros(count, np.uint16)
+        assert lib.qs_host_pack_u16(ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(dst.ctypes.data),
+                                    count) == 0
+        assert np.array_equal(dst, np.minimum(src, 65535).astype(np.uint16))
+    for count in (0, 1, 7, 8, 9, 1000, 4099):
+        x = rng.standard_normal(count).astype(np.float32).astype(np.float64)
+        out = np.zeros(count, np.float32)
+        ok = ctypes.c_int(-1)
+        lib.qs_host_pack_f32(ctypes.c_void_p(x.ctypes.data), ctypes.c_void_p(out.ctypes.data), count,
+                             ctypes.byref(ok))
+        assert ok.value == 1 and np.array_equal(out.astype(np.float64), x)
+        if count:
+            for bad in (0.1, np.nan, 1e300):
+                y = x.copy()
+                y[count // 2] = bad
+                lib.qs_host_pack_f32(ctypes.c_void_p(y.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                                     count, ctypes.byref(ok))
+                assert ok.value == 0
+    buf = np.zeros(16, np.uint8)
+    assert lib.qs_host_ptr_pinned(ctypes.c_void_p(buf.ctypes.data)) == 0
+    assert lib.qs_host_ptr_pinned(None) == 0
