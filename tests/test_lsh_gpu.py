@@ -259,3 +259,33 @@ def test_host_bits_out_of_range(ls, bad_value):
     cfg = ls.SearchConfig(tables=100, hash_funcs=4, min_matches=5, near_repeat_exclusion_s=0.0)
     with pytest.raises(ParameterError):
         ls.search_fingerprints(fps, cfg)
+
+
+@pytest.mark.parametrize("n,K,d", [(1, 1, 64), (7, 3, 1000), (1001, 5, 70000), (4099, 37, 65535),
+                                   (5000, 400, 4096)])
+def test_host_transfer_shapes(ls, n, K, d, monkeypatch):
+    """Row widths that are not multiples of 16 bytes, one-row inputs and d
+    above the uint16 range (no narrowing) give the device path's signatures on
+    every host-transfer route, with chunks small enough to cycle the staging
+    buffers."""
+    import torch
+    from paper_1803_09835_b200 import minmax_hash as mh
+    rng = np.random.default_rng(n * 31 + K)
+    bits = np.sort(rng.integers(0, d, size=(n, K), dtype=np.uint32), axis=1)
+    m = mh.gen_hash_mapping(d, 12, 2, 3)
+    want = ls.signatures_for_search(torch.from_numpy(bits.view(np.int32)).cuda(), m)
+    hold = torch.empty(bits.shape, dtype=torch.int32, pin_memory=True)
+    hold.numpy()[...] = bits.view(np.int32)
+    for label, arr, env in (("pageable", bits.view(np.int32), {}),
+                            ("pageable_u32", bits.view(np.int32), {"QS_H2D_NARROW": "0"}),
+                            ("pinned", hold.numpy(), {}),
+                            ("pinned_all", hold.numpy(), {"QS_H2D_SPLIT": "1"}),
+                            ("pinned_direct", hold.numpy(), {"QS_H2D_SPLIT": "0"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        got = ls.signatures_for_search_host(arr, m, chunk_bytes=max(64, n * K * 4 // 5))
+        torch.cuda.synchronize()
+        for k in env:
+            monkeypatch.delenv(k)
+        for g, w in zip(got, want):
+            assert torch.equal(g, w), (label, n, K, d)

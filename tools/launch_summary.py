@@ -4,7 +4,7 @@ tools/one_search.py: per-kernel totals of the LAST search of the run (the first
 is the warm-up), and the pair-stage DRAM traffic written to profiles/traffic.json
 (the `roofline.traffic` bench.py reports).
 
-usage: launch_summary.py launches.csv [--half] [--traffic profiles/traffic.json] [--n 8000000]
+usage: launch_summary.py launches.csv [--half] [--div STEPS] [--traffic profiles/traffic.json] [--n 8000000]
 """
 import collections
 import csv
@@ -18,6 +18,7 @@ def main():
     half = "--half" in sys.argv
     traffic_out = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
     n = int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 8_000_000
+    div = float(sys.argv[sys.argv.index("--div") + 1]) if "--div" in sys.argv else 1.0  # steps in the run
     rows = [r for r in csv.reader(open(path, errors="replace")) if len(r) > 10]
     hdr = rows[0]
     ki, mi, vi, ii, ui = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID",
@@ -42,10 +43,15 @@ def main():
         a["ms"] += d.get("gpu__time_duration.sum", 0.0)
         a["inst"] += d.get("smsp__inst_executed.sum", 0.0)
         a["dram"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    for a in agg.values():
+        for k in ("n", "ms", "inst", "dram"):
+            a[k] = a[k] / div
     tot = sum(a["ms"] for a in agg.values())
+    if div != 1.0:
+        print(f"per step (totals of the run / {div:g} steps)")
     print(f"launches {len(launches)} in part {len(ls)} total ms {tot:.2f}")
     for k, a in sorted(agg.items(), key=lambda x: -x[1]["ms"]):
-        print(f"{k:50s} n={a['n']:5d} ms={a['ms']:8.2f} inst={a['inst']:.3g} dramGB={a['dram'] / 1e9:7.2f}")
+        print(f"{k:50s} n={a['n']:7.1f} ms={a['ms']:8.2f} inst={a['inst']:.3g} dramGB={a['dram'] / 1e9:7.2f}")
     if traffic_out:
         pair = {k: a for k, a in agg.items() if k.startswith("k_pairs_")}
         out = {"n": n, "kernel": "k_pairs_pc + k_pairs_small (every pair-stage launch of one cfg1 step)",
