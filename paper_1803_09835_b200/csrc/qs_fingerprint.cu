@@ -799,8 +799,11 @@ constexpr size_t WC_OFF_LL2 = WC_OFF_LL1 + 512 * 8, WC_OFF_LL3 = WC_OFF_LL2 + 12
 constexpr size_t WC_OFF_TAB = WC_OFF_LL3 + 64 * 8;
 constexpr size_t WC_SMEM = WC_OFF_TAB + (32 * WC_FT + WC_NWID * 64 * WC_TT) * 12 + 64;
 
+#ifndef WC_MINB
+#define WC_MINB 4  // resident CTAs per SM asked of ptxas (A/B builds: make EXTRA=-DWC_MINB=5)
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(WC_T, 4) k_win_cta(
+__global__ void __launch_bounds__(WC_T, WC_MINB) k_win_cta(
     const float* __restrict__ band, WinGeom g, const int64_t* __restrict__ widx,
     const int32_t* __restrict__ wf_off, const int32_t* __restrict__ wf_idx,
     const double* __restrict__ wf_val, const int32_t* __restrict__ wt_off,

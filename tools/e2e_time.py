@@ -39,7 +39,7 @@ def run(host_bits, label, env):
 
 
 hp = pin.numpy().view(np.uint32)
-for sp in ("0", "0.5", "0.7", "0.8", "0.9", "1"):
+for sp in os.environ.get("QS_E2E_SPLITS", "0,0.5,0.7,0.8,0.9,1").split(","):
     run(hp, f"pinned split={sp}", {"QS_H2D_SPLIT": sp})
 pg = np.array(hp)
 for thr_env in ({}, {"QS_H2D_NARROW": "0"}):
