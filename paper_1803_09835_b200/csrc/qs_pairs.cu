@@ -297,7 +297,13 @@ struct Queue {
 
 // Drain `cnt` (<= 32) queued candidates, one per lane: first-table rule on
 // the candidate bits below the table, confirmed count on the bits above.
-template <int W>
+// Every launch covers one table word (wt == WT), so the word loops have
+// compile-time bounds; they stay rolled (one copy of each confirmation loop
+// per call site instead of W: the kernel's code shrinks by half, and with it
+// the instruction-fetch stalls of the warps that enter a drain), and the
+// unexamined candidate words of a lazy count go back into the lane's own
+// queue slot instead of a register array.
+template <int W, int WT>
 __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cnt, uint32_t lane,
                                       const uint64_t* __restrict__ rkeys, uint32_t t, uint32_t m,
                                       uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim,
@@ -310,15 +316,18 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
         const uint32_t a = q.qa[e], b = q.qb[e], f = q.qt[e];
         QS_DASSERT(a < b);
         const uint32_t table = (f & 0xFFu) | ((f >> 16) << 8);
-        const int wt = (int)(table >> 5);
+        QS_DASSERT((int)(table >> 5) == WT);
         const uint32_t bt = table & 31, low = (1u << bt) - 1u;
+        uint32_t* qm = q.qm + e * W;
         bool first = true;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            if (w > wt || !first) break;
-            const uint32_t mw = q.qm[e * W + w];
-            const uint32_t ebits = (w < wt) ? mw : (mw & low);
-            if (ebits && confirm(rkeys, t, a, b, ebits, w * 32, true)) first = false;
+#pragma unroll 1
+        for (int w = 0; w <= WT; ++w) {
+            const uint32_t mw = qm[w];
+            const uint32_t ebits = (w < WT) ? mw : (mw & low);
+            if (ebits && confirm(rkeys, t, a, b, ebits, w * 32, true)) {
+                first = false;
+                break;
+            }
         }
         if (first) {
             if (f & QF_DISTINCT) ++distinct;
@@ -328,16 +337,13 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
                 // exact count is completed only for pairs the filter keeps
                 const bool lazy = out_rest != nullptr;
                 uint32_t exact = 1;
-                uint32_t rest[W];
-#pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    rest[w] = 0;
-                    if (w < wt) continue;
-                    const uint32_t mw = q.qm[e * W + w];
-                    uint32_t x = (w == wt) ? (mw & ~((low << 1) | 1u)) : mw;
+#pragma unroll 1
+                for (int w = WT; w < W; ++w) {
+                    const uint32_t mw = qm[w];
+                    uint32_t x = (w == WT) ? (mw & ~((low << 1) | 1u)) : mw;
                     if (lazy) {
                         if (x && exact < m) exact += confirm_upto(rkeys, t, a, b, x, w * 32, m - exact);
-                        rest[w] = x;
+                        qm[w] = x;
                     } else if (x) {
                         exact += confirm(rkeys, t, a, b, x, w * 32, false);
                     }
@@ -349,7 +355,7 @@ __device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cn
                         out_sim[pos] = exact;
                         if (lazy) {
 #pragma unroll
-                            for (int w = 0; w < W; ++w) out_rest[pos * W + w] = rest[w];
+                            for (int w = 0; w < W; ++w) out_rest[pos * W + w] = w < WT ? 0u : qm[w];
                         }
                     }
                 }
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                         __syncwarp();
                         PROF_STOP(1)
                         PROF_START
-                        drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
+                        drain<W, WT>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
                                  counters, distinct);
                         PROF_STOP(2)
                         PROF_START
@@ -969,7 +975,7 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
         if (lane == 0) mbar_arrive(&empty_bar[bsel]);
     }
     __syncwarp();
-    if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
+    if (qn) drain<W, WT>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
                      distinct);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);
@@ -1253,7 +1259,7 @@ __global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) 
                 qn += __popc(bal);
                 if (qn >= 32) {
                     __syncwarp();
-                    drain<W>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
+                    drain<W, WT>(q, qhead, 32, lane, rkeys, t, m, out_key, out_sim, out_rest, cap,
                              counters, distinct);
                     qhead = (qhead + 32) & (QCAP - 1);
                     qn -= 32;
@@ -1269,7 +1275,7 @@ __global__ void __launch_bounds__(SM_WARPS * 32, (SmallCfg<W, MODE, WT>::MINB)) 
         a0 = a1; a1 = a2;
     }
     __syncwarp();
-    if (qn) drain<W>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
+    if (qn) drain<W, WT>(q, qhead, qn, lane, rkeys, t, m, out_key, out_sim, out_rest, cap, counters,
                      distinct);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, o);

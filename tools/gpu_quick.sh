@@ -1,7 +1,16 @@
-# quick GPU iteration: parity tests of the search + timed bench without the CPU/e2e/fingerprint legs
-cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_lsh_gpu.py tests/test_sharded_gpu.py -x -q > gpurun_out/pt_q.log 2>&1; tail -2 gpurun_out/pt_q.log
-timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-fingerprint > gpurun_out/b_q.log 2>&1; tail -1 gpurun_out/b_q.log | python3 -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], {k: round(v,1) for k,v in l['stages_ms'].items()}, l['roofline']['frac'])"
-if [ -n "$QS_N2" ]; then
-QS_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --fingerprints 2000000 --no-cpu-baseline --no-fingerprint > gpurun_out/b_n2.log 2>&1; echo n2 $?; tail -1 gpurun_out/b_n2.log | cut -c1-1200
-fi
+#!/bin/bash
+# quick check of a search-path change: search tests, a short randomised sweep, a short bench (stage split)
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out; O=gpurun_out; T=${1:-q}
+timeout 1200 python -m pytest tests/test_lsh_gpu.py tests/test_capi_search_gpu.py tests/test_sharded_gpu.py -q -x -p no:cacheprovider -k "not full_scale" 2>&1 | tail -2 | tee $O/${T}_pytest.log
+timeout 900 python tools/stress_parity.py 60 2>&1 | tail -1 | tee $O/${T}_stress.log
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-fingerprint --full-steps 1 > $O/${T}_bench.log 2>&1; echo "bench rc=$?"
+python - "$O/${T}_bench.log" <<'PY'
+import json, sys
+for l in open(sys.argv[1]):
+    if l.startswith('{'):
+        j = json.loads(l)
+        print('ms/step', round(j['ms_per_step'], 2), {k: round(v, 1) for k, v in j['stages_ms'].items()})
+        if j.get('full_mode'):
+            print('full ms/step', round(j['full_mode']['ms_per_step'], 2), {k: round(v, 1) for k, v in j['full_mode']['stages_ms'].items()})
+        print('triplets', j['emitted_triplets'], 'filtered', j['filtered_fingerprints'], 'distinct', j['distinct_pairs'])
+PY
