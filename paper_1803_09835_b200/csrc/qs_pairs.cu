@@ -303,8 +303,11 @@ struct Queue {
 // the instruction-fetch stalls of the warps that enter a drain), and the
 // unexamined candidate words of a lazy count go back into the lane's own
 // queue slot instead of a register array.
+#ifndef QS_DRAIN_INLINE
+#define QS_DRAIN_INLINE __forceinline__
+#endif
 template <int W, int WT>
-__device__ __forceinline__ void drain(const Queue& q, uint32_t base, uint32_t cnt, uint32_t lane,
+__device__ QS_DRAIN_INLINE void drain(const Queue& q, uint32_t base, uint32_t cnt, uint32_t lane,
                                       const uint64_t* __restrict__ rkeys, uint32_t t, uint32_t m,
                                       uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_sim,
                                       uint32_t* __restrict__ out_rest,
@@ -923,7 +926,32 @@ __global__ void __launch_bounds__(PTHREADS, TileCfg<W, MODE, WT>::MINB) k_pairs_
                     }
                 }
             };
-            if (FOLD && tri) {
+#ifndef QS_PAIR_MERGED
+#define QS_PAIR_MERGED 0
+#endif
+            if (QS_PAIR_MERGED && FOLD && MODE != MODE_DISTINCT) {
+                // one loop (one copy of eval / push / drain in the kernel) for fold
+                // and rectangular chunks: the step's row is per-lane in a fold
+                // chunk and the same for every lane otherwise
+                const bool fold = tri;
+                const uint32_t nst = fold ? (acnt >> 1) : (bend > bbeg ? bend - bbeg : 0u);
+                for (uint32_t st = 0; st < nst; ++st) {
+                    uint32_t u = bbeg + st;
+                    bool ok = false;
+                    if (fold) {
+                        const uint32_t dd = st + 1;
+                        uint32_t j = lane + dd;
+                        if (j >= acnt) j -= acnt;
+                        ok = active && (2 * dd != acnt || lane < dd);
+                        u = abase + (active ? j : 0);
+                    }
+                    const uint32_t* R = rows + u * C::ROWP;
+                    bool s0;
+                    uint32_t f0, m0[W];
+                    eval(u, R, fold, ok, s0, f0, m0);
+                    push(u, R, fold, s0, f0, m0);
+                }
+            } else if (FOLD && tri) {
                 // fold chunk: the pairs among the chunk's own acnt rows, lane i
                 // against row i + dd (mod acnt); at dd = acnt / 2 (even acnt) the
                 // lanes i < dd cover every pair once
