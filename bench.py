@@ -626,7 +626,7 @@ def run_ours(args):
         # the step's inputs in PINNED host memory (the bench contract): the library
         # detects page-locked arrays and copies them by DMA from where they lie; the
         # same call with a pageable numpy array (staged through pinned buffers,
-        # narrowed to uint16 on the way) is reported as `pageable`
+        # narrowed to 12-bit fields on the way) is reported as `pageable`
         src = bits[: host_rows[1] - host_rows[0]] if tables_mode else bits
         pinned_t = torch.empty(tuple(src.shape), dtype=torch.int32, pin_memory=True)
         pinned_t.copy_(src)
@@ -669,7 +669,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(out_bytes), "input_bytes_per_step": int(e_units * 400 * 4),
                "seconds_per_step": e_s,
                "host_memory": ("pinned: DMA from the caller's array, QS_H2D_SPLIT (default 0.7) of "
-                               "every chunk's rows narrowed to uint16 by the host cores on the way "
+                               "every chunk's rows narrowed to 12-bit fields (d = 4096) by the host cores on the way "
                                "(h2d_bytes_per_step = the bytes that crossed PCIe)"),
                "path": ("sharded.search_fingerprints_sharded (host row block per rank)" if tables_mode
                         else "lsh_search.search_fingerprints(FingerprintSet with host numpy bits)")}
@@ -680,8 +680,8 @@ def run_ours(args):
             e2e["pageable"] = {"value": e_units / p_s, "seconds_per_step": p_s,
                                "h2d_bytes_per_step": ph2d,
                                "host_memory": ("pageable numpy array: staged through two pinned "
-                                               "buffers by a thread pool, narrowed to uint16 on the "
-                                               "way (qs_host_pack_u16), widened on the device")}
+                                               "buffers by a thread pool, narrowed to 12-bit fields "
+                                               "on the way (qs_host_pack_u12), widened on the device")}
             del pageable
         else:
             del pinned_t

@@ -54,12 +54,19 @@ int qs_host_ptr_pinned(const void* host_ptr);
  * staged (valid for d <= 65535: a saturated value is >= d and is flagged by
  * the signature kernel's range check).  Host function, thread-safe. */
 int qs_host_pack_u16(const uint32_t* src_host, uint16_t* dst_host, uint64_t count);
+/* The same with 12-bit fields (value i in bits [12 i, 12 i + 12) of the byte
+ * stream, ceil(1.5 count) bytes) for d <= 4096; *fits_out = 0 when a value
+ * above 4095 was seen (the caller then uses the uint16 route for that chunk).
+ * Host function, thread-safe. */
+int qs_host_pack_u12(const uint32_t* src_host, uint8_t* dst_host, uint64_t count, int* fits_out);
 /* dst_host[i] = (float)src_host[i]; *exact_out = 1 when every value widens
  * back to itself (then a float32 upload gives the chain the same samples),
  * 0 otherwise (NaN, overflow, inexact).  Host function, thread-safe. */
 int qs_host_pack_f32(const double* src_host, float* dst_host, uint64_t count, int* exact_out);
 /* dst_dev[i] = src_dev[i] (uint16 -> uint32), both 16-byte aligned. */
 int qs_bits_widen_u16(const uint16_t* src_dev, uint32_t* dst_dev, uint64_t count, void* stream);
+/* dst_dev[i] = field i of the 12-bit stream (src 4-byte, dst 16-byte aligned). */
+int qs_bits_widen_u12(const uint8_t* src_dev, uint32_t* dst_dev, uint64_t count, void* stream);
 int qs_memcpy_h2d_async(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 int qs_memcpy_d2h_async(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 

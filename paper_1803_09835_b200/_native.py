@@ -51,8 +51,10 @@ SIGNATURES = {
     "qs_device_info": (_int, [ctypes.c_char_p, _sz]),
     "qs_host_ptr_pinned": (_int, [_p]),
     "qs_host_pack_u16": (_int, [_p, _p, _u64]),
+    "qs_host_pack_u12": (_int, [_p, _p, _u64, ctypes.POINTER(ctypes.c_int)]),
     "qs_host_pack_f32": (_int, [_p, _p, _u64, ctypes.POINTER(ctypes.c_int)]),
     "qs_bits_widen_u16": (_int, [_p, _p, _u64, _p]),
+    "qs_bits_widen_u12": (_int, [_p, _p, _u64, _p]),
     "qs_memcpy_h2d_async": (_int, [_p, _p, _sz, _p]),
     "qs_memcpy_d2h_async": (_int, [_p, _p, _sz, _p]),
     "qs_gen_hash_mapping": (_int, [_p, _u32, _u32, _u64, _p]),

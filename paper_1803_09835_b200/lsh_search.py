@@ -729,9 +729,11 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
     landed.  A page-locked array is copied by DMA straight from the caller's
     memory; a pageable one goes through two pinned staging buffers (the host
     pass into one buffer split over a thread pool while the other's DMA runs),
-    narrowed to uint16 on the way when d <= 65535 (qs_host_pack_u16: half the
-    staging writes and half the DMA bytes; widened again on the device,
-    out-of-range values saturate and are flagged by the kernel's range check)."""
+    narrowed on the way: to 12-bit fields when d <= 4096 (qs_host_pack_u12: 3/8
+    of the staging writes and DMA bytes; a chunk holding an index above 4095
+    switches the call to the uint16 route), to uint16 when d <= 65535
+    (qs_host_pack_u16: half the bytes; out-of-range values saturate and are
+    flagged by the kernel's range check); widened again on the device."""
     torch = nat.torch()
     n, K = arr.shape
     t = mapping.t
@@ -754,114 +756,119 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
                  mapping.d, t, mapping.k_half, None, nat.ptr(keys), nat.ptr(rkeys), nat.ptr(tags),
                  nat.ptr(bad), nat.stream())
 
-    narrow = mapping.d <= 0xFFFF and os.environ.get("QS_H2D_NARROW", "1") != "0"
-    if _host_pinned(arr):
+    # field width of the narrowed rows: 12 bits when every index fits (d <= 4096
+    # and an even K, so that row ranges start on byte boundaries), else 16 bits
+    # (d <= 65535), else none.  QS_H2D_NARROW = 0 / 16 / 12 caps it.
+    level = os.environ.get("QS_H2D_NARROW", "12")  # "0": off, "16" (or "1"): uint16 only
+    width = 0
+    if mapping.d <= 0xFFFF and level != "0":
+        width = 16
+    if mapping.d <= 4096 and K % 2 == 0 and level not in ("0", "1", "16"):
+        width = 12
+    pinned_src = _host_pinned(arr)
+    src_base = arr.ctypes.data if pinned_src else arr.view(np.uint32).ctypes.data
+    split = 1.0
+    if pinned_src:
         # DMA from the caller's memory.  With narrowing on, the first `split` of
-        # every chunk's rows is narrowed to uint16 by the thread pool (into pinned
-        # staging buffers, for the next chunk while this one's copies run) and the
-        # rest is copied as it lies: the PCIe link then moves (1 - split / 2) of the
-        # bytes while the host cores stay below their own narrowing rate
-        # (QS_H2D_SPLIT, default 0.7: measured on the 16-core B200 box, where the
-        # cores narrow ~67 GB/s of source and the link copies ~55 GB/s).
-        base = arr.ctypes.data
-        split = float(os.environ.get("QS_H2D_SPLIT", "0.7")) if narrow else 0.0
+        # every chunk's rows is narrowed by the thread pool (into pinned staging
+        # buffers, for the next chunk while this one's copies run) and the rest is
+        # copied as it lies: the PCIe link then moves fewer bytes while the host
+        # cores stay below their own narrowing rate (QS_H2D_SPLIT, default 0.7:
+        # measured on the 16-core B200 box, where the cores narrow ~67 GB/s of
+        # source and the link copies ~55 GB/s).
+        split = float(os.environ.get("QS_H2D_SPLIT", "0.7")) if width else 0.0
         split = min(1.0, max(0.0, split))
-        pool = _copy_pool()
-        nthr = pool._max_workers
-        cap = min(rows_per, n)
-        ncap = int(cap * split)
-        if ncap:
-            stage = [torch.empty((ncap, K), dtype=torch.int16, pin_memory=True) for _ in range(2)]
-            dstage = [torch.empty((ncap, K), dtype=torch.int16, device="cuda") for _ in range(2)]
-        done = [None, None]
-        for k, r0 in enumerate(range(0, n, rows_per)):
-            rows = min(n, r0 + rows_per) - r0
-            nrow = min(ncap, int(rows * split))
-            sl = k & 1
-            if nrow:
-                if done[sl] is not None:
-                    done[sl].synchronize()
-                step = max(1, (1 << 18) // K, -(-nrow // nthr))
-                hbase = stage[sl].data_ptr()
-
-                def pack(i, r0=r0, nrow=nrow, hbase=hbase, step=step):
-                    cnt = min(nrow, i + step) - i
-                    lib.qs_host_pack_u16(nat.ctypes.c_void_p(base + (r0 + i) * K * 4),
-                                         nat.ctypes.c_void_p(hbase + i * K * 2), cnt * K)
-
-                list(pool.map(pack, range(0, nrow, step)))
-                with torch.cuda.stream(copy):
-                    dstage[sl][:nrow].copy_(stage[sl][:nrow], non_blocking=True)
-                nat.call("qs_bits_widen_u16", nat.ptr(dstage[sl]),
-                         nat.ctypes.c_void_p(bdev.data_ptr() + r0 * K * 4), nrow * K, cstream)
-            LAST_H2D_BYTES += nrow * K * 2 + (rows - nrow) * K * 4
-            if rows > nrow:
-                nat.call("qs_memcpy_h2d_async",
-                         nat.ctypes.c_void_p(bdev.data_ptr() + (r0 + nrow) * K * 4),
-                         nat.ctypes.c_void_p(base + (r0 + nrow) * K * 4), (rows - nrow) * K * 4,
-                         cstream)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-            done[sl] = ev
-            compute.wait_event(ev)
-            sign(r0, rows)
-        bdev.record_stream(copy)
-        if ncap:
-            for d_ in dstage:
-                d_.record_stream(copy)
-        # the caller's array is read until the last copy has run: the search that
-        # follows synchronises (the range flag's .item()) before anything returns
-        return keys, rkeys, tags, bad
-
     pool = _copy_pool()
     nthr = pool._max_workers
     cap = min(rows_per, n)
+    ncap = int(cap * split) if width else (0 if pinned_src else cap)
+    state = {"width": width, "stage": None, "dstage": None}
+
+    def alloc(w):
+        # two pinned staging buffers (+ their device twins when the rows are narrowed)
+        if ncap == 0:
+            return
+        row_bytes = K * 4 if w == 0 else (K * 2 if w == 16 else K * 3 // 2)
+        nbytes = (ncap * row_bytes + 15) & ~15
+        state["stage"] = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        state["dstage"] = ([torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+                           if w else None)
+        state["width"] = w
+
+    alloc(width)
     done = [None, None]
-    if narrow:
-        stage = [torch.empty((cap, K), dtype=torch.int16, pin_memory=True) for _ in range(2)]
-        dstage = [torch.empty((cap, K), dtype=torch.int16, device="cuda") for _ in range(2)]
-        src = arr.view(np.uint32)
-    else:
-        stage = [torch.empty((cap, K), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+
+    def pack_rows(w, r0, nrow, hbase):
+        """Rows [r0, r0 + nrow) into the staging buffer at hbase, split over the
+        pool; False when a 12-bit pack met a value above 4095."""
+        step = max(1, (1 << 18) // K, -(-nrow // nthr))
+        if w == 12 and step % 2:
+            step += 1  # even row counts keep every task's start on a byte boundary for any even K
+        fits = [True]
+
+        def one(i):
+            cnt = min(nrow, i + step) - i
+            sp = nat.ctypes.c_void_p(src_base + (r0 + i) * K * 4)
+            if w == 12:
+                ok = nat.ctypes.c_int(1)
+                lib.qs_host_pack_u12(sp, nat.ctypes.c_void_p(hbase + i * K * 3 // 2), cnt * K,
+                                     nat.ctypes.byref(ok))
+                if not ok.value:
+                    fits[0] = False
+            elif w == 16:
+                lib.qs_host_pack_u16(sp, nat.ctypes.c_void_p(hbase + i * K * 2), cnt * K)
+            else:
+                nat.ctypes.memmove(hbase + i * K * 4, sp, cnt * K * 4)
+
+        list(pool.map(one, range(0, nrow, step)))
+        return fits[0]
+
     for k, r0 in enumerate(range(0, n, rows_per)):
-        r1 = min(n, r0 + rows_per)
+        rows = min(n, r0 + rows_per) - r0
+        nrow = min(ncap, int(rows * split)) if pinned_src else rows
         sl = k & 1
-        if done[sl] is not None:
-            done[sl].synchronize()
-        rows = r1 - r0
-        step = max(1, (1 << 18) // K, -(-rows // nthr))
-        if narrow:
-            hbase = stage[sl].data_ptr()
-
-            def pack(i, r0=r0, rows=rows, hbase=hbase):
-                cnt = min(rows, i + step) - i
-                lib.qs_host_pack_u16(nat.ctypes.c_void_p(src.ctypes.data + (r0 + i) * K * 4),
-                                     nat.ctypes.c_void_p(hbase + i * K * 2), cnt * K)
-
-            list(pool.map(pack, range(0, rows, step)))
+        if nrow:
+            if done[sl] is not None:
+                done[sl].synchronize()
+            w = state["width"]
+            if not pack_rows(w, r0, nrow, state["stage"][sl].data_ptr()):
+                # an index above 4095 (invalid for this d): this and the later chunks
+                # take the uint16 route, whose saturated values the kernel flags
+                for ev_ in done:
+                    if ev_ is not None:
+                        ev_.synchronize()
+                alloc(16)
+                w = 16
+                pack_rows(16, r0, nrow, state["stage"][sl].data_ptr())
+            row_bytes = K * 4 if w == 0 else (K * 2 if w == 16 else K * 3 // 2)
+            st_, dst_ = state["stage"][sl], bdev.data_ptr() + r0 * K * 4
             with torch.cuda.stream(copy):
-                dstage[sl][:rows].copy_(stage[sl][:rows], non_blocking=True)
-                nat.call("qs_bits_widen_u16", nat.ptr(dstage[sl]),
-                         nat.ctypes.c_void_p(bdev.data_ptr() + r0 * K * 4), rows * K, cstream)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-        else:
-            host = stage[sl].numpy()
-            list(pool.map(lambda i: np.copyto(host[i:min(rows, i + step)],
-                                              arr[r0 + i:r0 + min(rows, i + step)]),
-                          range(0, rows, step)))
-            with torch.cuda.stream(copy):
-                bdev[r0:r1].copy_(stage[sl][:rows], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
+                if w == 0:
+                    nat.call("qs_memcpy_h2d_async", nat.ctypes.c_void_p(dst_),
+                             nat.ctypes.c_void_p(st_.data_ptr()), nrow * row_bytes, cstream)
+                else:
+                    dv = state["dstage"][sl]
+                    dv[:nrow * row_bytes].copy_(st_[:nrow * row_bytes], non_blocking=True)
+                    nat.call("qs_bits_widen_u16" if w == 16 else "qs_bits_widen_u12", nat.ptr(dv),
+                             nat.ctypes.c_void_p(dst_), nrow * K, cstream)
+            LAST_H2D_BYTES += nrow * row_bytes
+        if rows > nrow:  # the rest of a page-locked chunk by DMA from where it lies
+            nat.call("qs_memcpy_h2d_async",
+                     nat.ctypes.c_void_p(bdev.data_ptr() + (r0 + nrow) * K * 4),
+                     nat.ctypes.c_void_p(src_base + (r0 + nrow) * K * 4), (rows - nrow) * K * 4,
+                     cstream)
+            LAST_H2D_BYTES += (rows - nrow) * K * 4
+        ev = torch.cuda.Event()
+        ev.record(copy)
         done[sl] = ev
         compute.wait_event(ev)
         sign(r0, rows)
-        LAST_H2D_BYTES += rows * K * (2 if narrow else 4)
     bdev.record_stream(copy)
-    if narrow:
-        for d_ in dstage:
+    if state["dstage"]:
+        for d_ in state["dstage"]:
             d_.record_stream(copy)
+    # a page-locked caller array is read until the last copy has run: the search
+    # that follows synchronises (the range flag's .item()) before anything returns
     return keys, rkeys, tags, bad
 
 

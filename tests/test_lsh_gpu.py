@@ -262,7 +262,8 @@ def test_host_bits_out_of_range(ls, bad_value):
 
 
 @pytest.mark.parametrize("n,K,d", [(1, 1, 64), (7, 3, 1000), (1001, 5, 70000), (4099, 37, 65535),
-                                   (5000, 400, 4096)])
+                                   (5000, 400, 4096), (1, 2, 4096), (1001, 6, 4096), (333, 10, 17),
+                                   (4099, 38, 4095)])
 def test_host_transfer_shapes(ls, n, K, d, monkeypatch):
     """Row widths that are not multiples of 16 bytes, one-row inputs and d
     above the uint16 range (no narrowing) give the device path's signatures on
@@ -278,6 +279,8 @@ def test_host_transfer_shapes(ls, n, K, d, monkeypatch):
     hold.numpy()[...] = bits.view(np.int32)
     for label, arr, env in (("pageable", bits.view(np.int32), {}),
                             ("pageable_u32", bits.view(np.int32), {"QS_H2D_NARROW": "0"}),
+                            ("pageable_u16", bits.view(np.int32), {"QS_H2D_NARROW": "16"}),
+                            ("pinned_u16", hold.numpy(), {"QS_H2D_NARROW": "16", "QS_H2D_SPLIT": "1"}),
                             ("pinned", hold.numpy(), {}),
                             ("pinned_all", hold.numpy(), {"QS_H2D_SPLIT": "1"}),
                             ("pinned_direct", hold.numpy(), {"QS_H2D_SPLIT": "0"})):
@@ -289,3 +292,31 @@ def test_host_transfer_shapes(ls, n, K, d, monkeypatch):
             monkeypatch.delenv(k)
         for g, w in zip(got, want):
             assert torch.equal(g, w), (label, n, K, d)
+
+
+@pytest.mark.parametrize("host_memory", ["pageable", "pinned"])
+def test_host_bits_12bit_fallback_mid_call(ls, host_memory, monkeypatch):
+    """d = 4096 rows go up as 12-bit fields; an index above 4095 in a later chunk
+    (invalid for this d) switches the call to the uint16 route, and the range
+    flag is raised exactly as on the device path."""
+    import torch
+    from paper_1803_09835_b200 import minmax_hash as mh
+    rng = np.random.default_rng(11)
+    n, K, d = 3000, 8, 4096
+    bits = np.sort(rng.integers(0, d, size=(n, K), dtype=np.uint32), axis=1)
+    bits[2500, 3] = 5000
+    m = mh.gen_hash_mapping(d, 12, 2, 3)
+    want = ls.signatures_for_search(torch.from_numpy(bits.view(np.int32)).cuda(), m)
+    arr = bits.view(np.int32)
+    if host_memory == "pinned":
+        hold = torch.empty(bits.shape, dtype=torch.int32, pin_memory=True)
+        hold.numpy()[...] = arr
+        arr = hold.numpy()
+        monkeypatch.setenv("QS_H2D_SPLIT", "1")
+    got = ls.signatures_for_search_host(arr, m, chunk_bytes=n * K * 4 // 6)
+    torch.cuda.synchronize()
+    assert int(got[3].item()) == int(want[3].item()) == 1  # the range flag
+    ok = np.ones(n, bool)
+    ok[2500] = False
+    okt = torch.from_numpy(ok).cuda()
+    assert torch.equal(got[1][okt], want[1][okt])  # row-major keys of the valid rows

@@ -56,6 +56,32 @@ def test_host_pack_helpers():
         assert lib.qs_host_pack_u16(ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(dst.ctypes.data),
                                     count) == 0
         assert np.array_equal(dst, np.minimum(src, 65535).astype(np.uint16))
+    # 12-bit fields: value i in bits [12 i, 12 i + 12) of the byte stream
+    for count in (0, 1, 2, 7, 8, 15, 16, 17, 24, 31, 1000, 4099):
+        src = rng.integers(0, 4096, count, dtype=np.uint32)
+        nbytes = (count * 12 + 7) // 8
+        dst = np.full(nbytes + 8, 0xAA, np.uint8)  # the guard bytes must stay untouched
+        ok = ctypes.c_int(-1)
+        assert lib.qs_host_pack_u12(ctypes.c_void_p(src.ctypes.data), ctypes.c_void_p(dst.ctypes.data),
+                                    count, ctypes.byref(ok)) == 0
+        assert ok.value == 1
+        want = np.zeros(nbytes + 2, np.uint8)
+        for i, v in enumerate(src.tolist()):
+            bit = 12 * i
+            word = int(v) << (bit & 7)
+            want[bit >> 3] |= word & 0xFF
+            want[(bit >> 3) + 1] |= (word >> 8) & 0xFF
+            if word >> 16:
+                want[(bit >> 3) + 2] |= word >> 16
+        assert np.array_equal(dst[:nbytes], want[:nbytes]), count
+        assert np.all(dst[nbytes:] == 0xAA), count
+        if count:
+            for pos in {0, count // 2, count - 1}:
+                bad = src.copy()
+                bad[pos] = 4096
+                lib.qs_host_pack_u12(ctypes.c_void_p(bad.ctypes.data), ctypes.c_void_p(dst.ctypes.data),
+                                     count, ctypes.byref(ok))
+                assert ok.value == 0, (count, pos)
     for count in (0, 1, 7, 8, 9, 1000, 4099):
         x = rng.standard_normal(count).astype(np.float32).astype(np.float64)
         out = np.zeros(count, np.float32)
