@@ -339,11 +339,12 @@ def fingerprint_bench(args, steps, device, threads, cpu=True):
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(steps):
-        fps, mad = fp.fingerprint_series(ts, params, mad_rate=0.1)
-    b.record()
-    torch.cuda.synchronize()
+    with ClockSampler(device.index or 0) as fclk:  # the FP64-heavy chain has its own clocks line
+        a.record()
+        for _ in range(steps):
+            fps, mad = fp.fingerprint_series(ts, params, mad_rate=0.1)
+        b.record()
+        torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     n_fp = int(fps.bits.shape[0])
     del fps
@@ -363,6 +364,7 @@ def fingerprint_bench(args, steps, device, threads, cpu=True):
     out = {"metric": "fingerprint Msamples/s", "value": n / ms / 1e3, "unit": "Msamples/s",
            "ms_per_step": ms, "steps": steps, "n_samples": n, "n_fingerprints": n_fp,
            "workload": workload, "dtype": "f64 (STFT/resize/Haar/normalise), f32 stores",
+           "clocks": fclk.summary(),
            "e2e": {"value": n / e2e_s / 1e6, "unit": "Msamples/s", "seconds": e2e_s,
                    "h2d_bytes_per_step": int(n * 4), "d2h_bytes_per_step": d2h,
                    "host_memory": ("pageable float64 (TimeSeries coerces the float32 recording like "
