@@ -670,9 +670,12 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d or int(e_units * 400 * 4),
                "d2h_bytes_per_step": int(out_bytes), "input_bytes_per_step": int(e_units * 400 * 4),
                "seconds_per_step": e_s,
-               "host_memory": ("pinned: DMA from the caller's array, QS_H2D_SPLIT (default 0.7) of "
-                               "every chunk's rows narrowed to 12-bit fields (d = 4096) by the host cores on the way "
-                               "(h2d_bytes_per_step = the bytes that crossed PCIe)"),
+               "host_memory": ("pinned: DMA from the caller's array, a share of every chunk's rows "
+                               "(balanced during the call against the measured pack and copy "
+                               "rates, narrowed_share) narrowed to 12-bit fields (d = 4096) by the "
+                               "host cores on the way (h2d_bytes_per_step = the bytes that crossed "
+                               "PCIe)"),
+               "narrowed_share": round(float(ls.LAST_H2D_SPLIT), 3),
                "path": ("sharded.search_fingerprints_sharded (host row block per rank)" if tables_mode
                         else "lsh_search.search_fingerprints(FingerprintSet with host numpy bits)")}
         if not tables_mode:

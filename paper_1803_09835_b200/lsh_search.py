@@ -15,6 +15,7 @@ csrc/qs_sort.cu); this module only validates, allocates device buffers
 
 import math
 import os
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -712,6 +713,7 @@ def signatures_for_search(bits, mapping: HashMapping, with_keys: bool = True):
 
 
 LAST_H2D_BYTES = 0  # bytes the last signatures_for_search_host call sent over PCIe
+LAST_H2D_SPLIT = 0.0  # narrowed share of a page-locked array's rows at the end of that call
 
 
 def _host_pinned(arr: np.ndarray) -> bool:
@@ -748,7 +750,7 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
     copy.wait_stream(compute)  # bdev's allocation is ordered on the compute stream
     cstream = nat.ctypes.c_void_p(copy.cuda_stream)
     lib = nat.lib()
-    global LAST_H2D_BYTES
+    global LAST_H2D_BYTES, LAST_H2D_SPLIT
     LAST_H2D_BYTES = 0
 
     def sign(r0, rows):
@@ -778,10 +780,20 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
         # source and the link copies ~55 GB/s).
         split = float(os.environ.get("QS_H2D_SPLIT", "0.7")) if width else 0.0
         split = min(1.0, max(0.0, split))
+    # Without an explicit QS_H2D_SPLIT the share follows the measured rates of
+    # the call itself: the staging pass takes a * s and the chunk's copies
+    # b * (w * s + 1 - s) (w = narrowed bytes per source byte), equal at
+    # s = b / (a + (1 - w) * b); a and b come from the host clock around the
+    # pack and CUDA events around the copies of the chunk two steps back.  The
+    # narrowing rate of the host cores and the DMA rate from the caller's pages
+    # both vary from box to box (0.46-0.55 s for the same cfg1 call at a fixed
+    # 0.7); every split gives identical bytes.
+    adaptive = pinned_src and width and "QS_H2D_SPLIT" not in os.environ
+    timing = [None, None]  # per staging slot: (split, pack seconds, start event, end event)
     pool = _copy_pool()
     nthr = pool._max_workers
     cap = min(rows_per, n)
-    ncap = int(cap * split) if width else (0 if pinned_src else cap)
+    ncap = (cap if adaptive else int(cap * split)) if width else (0 if pinned_src else cap)
     state = {"width": width, "stage": None, "dstage": None}
 
     def alloc(w):
@@ -797,6 +809,9 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
 
     alloc(width)
     done = [None, None]
+
+    def state_w():
+        return {12: 0.375, 16: 0.5}.get(state["width"], 1.0)
 
     def pack_rows(w, r0, nrow, hbase):
         """Rows [r0, r0 + nrow) into the staging buffer at hbase, split over the
@@ -825,11 +840,20 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
 
     for k, r0 in enumerate(range(0, n, rows_per)):
         rows = min(n, r0 + rows_per) - r0
-        nrow = min(ncap, int(rows * split)) if pinned_src else rows
         sl = k & 1
+        if done[sl] is not None:
+            done[sl].synchronize()
+            if adaptive and timing[sl] is not None:
+                s_k, tp, e0, e1 = timing[sl]
+                td = e0.elapsed_time(e1) * 1e-3
+                if s_k > 0 and tp > 0 and td > 0:
+                    a_ = tp / s_k
+                    b_ = td / (state_w() * s_k + 1.0 - s_k)
+                    split = 0.5 * split + 0.5 * min(1.0, max(0.3, b_ / (a_ + (1.0 - state_w()) * b_)))
+                timing[sl] = None
+        nrow = min(ncap, int(rows * split)) if pinned_src else rows
+        t_pack0 = time.perf_counter()
         if nrow:
-            if done[sl] is not None:
-                done[sl].synchronize()
             w = state["width"]
             if not pack_rows(w, r0, nrow, state["stage"][sl].data_ptr()):
                 # an index above 4095 (invalid for this d): this and the later chunks
@@ -840,6 +864,10 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
                 alloc(16)
                 w = 16
                 pack_rows(16, r0, nrow, state["stage"][sl].data_ptr())
+            if adaptive:
+                t_pack = time.perf_counter() - t_pack0
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record(copy)  # this chunk's copies start here (or when the stream frees up)
             row_bytes = K * 4 if w == 0 else (K * 2 if w == 16 else K * 3 // 2)
             st_, dst_ = state["stage"][sl], bdev.data_ptr() + r0 * K * 4
             with torch.cuda.stream(copy):
@@ -858,11 +886,14 @@ def signatures_for_search_host(arr: np.ndarray, mapping: HashMapping, chunk_byte
                      nat.ctypes.c_void_p(src_base + (r0 + nrow) * K * 4), (rows - nrow) * K * 4,
                      cstream)
             LAST_H2D_BYTES += (rows - nrow) * K * 4
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=bool(adaptive))
         ev.record(copy)
         done[sl] = ev
+        if adaptive and nrow and rows == rows_per:
+            timing[sl] = (nrow / rows, t_pack, ev0, ev)
         compute.wait_event(ev)
         sign(r0, rows)
+    LAST_H2D_SPLIT = split if pinned_src else 1.0
     bdev.record_stream(copy)
     if state["dstage"]:
         for d_ in state["dstage"]:

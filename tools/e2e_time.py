@@ -33,14 +33,14 @@ def run(host_bits, label, env):
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     print(f"{label:34s} min {min(ts):.4f} median {sorted(ts)[len(ts) // 2]:.4f} s  h2d {ls.LAST_H2D_BYTES / 1e9:.2f} GB "
-          f"triplets {len(rec)}", flush=True)
+          f"triplets {len(rec)} split {ls.LAST_H2D_SPLIT:.3f}", flush=True)
     for k in env:
         os.environ.pop(k, None)
 
 
 hp = pin.numpy().view(np.uint32)
 for sp in os.environ.get("QS_E2E_SPLITS", "0,0.5,0.7,0.8,0.9,1").split(","):
-    run(hp, f"pinned split={sp}", {"QS_H2D_SPLIT": sp})
+    run(hp, f"pinned split={sp}", {} if sp == "auto" else {"QS_H2D_SPLIT": sp})
 pg = np.array(hp)
 for thr_env in ({}, {"QS_H2D_NARROW": "0"}):
     run(pg, f"pageable {thr_env or 'narrowed'}", thr_env)
